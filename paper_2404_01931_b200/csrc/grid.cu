@@ -1,0 +1,172 @@
+// grid.cu — face-lattice stages: body force + wall enforcement, pressure
+// gradient subtract, layered velocity extrapolation, divergence.
+#include "ops.cuh"
+
+namespace flip {
+
+struct Lat {
+    int mx, my, mz;
+};
+
+__host__ __device__ inline Lat lat(const Dims &d, int comp) {
+    if (comp == 0) return {d.nx + 1, d.ny, d.nz};
+    if (comp == 1) return {d.nx, d.ny + 1, d.nz};
+    return {d.nx, d.ny, d.nz + 1};
+}
+
+// Low/high cell of an interior face along its component axis; false on the
+// domain boundary.
+__device__ __forceinline__ bool face_cells(const Dims &d, int comp, int i, int j, int k,
+                                           int64_t &lo, int64_t &hi) {
+    int64_t sxy = (int64_t)d.nx * d.ny;
+    hi = i + (int64_t)j * d.nx + k * sxy;
+    if (comp == 0) {
+        if (i == 0 || i == d.nx) return false;
+        lo = hi - 1;
+    } else if (comp == 1) {
+        if (j == 0 || j == d.ny) return false;
+        lo = hi - d.nx;
+    } else {
+        if (k == 0 || k == d.nz) return false;
+        lo = hi - sxy;
+    }
+    return true;
+}
+
+// add_body_force (grid.py:193-202) then enforce_solid_boundaries (grid.py:219-228)
+// over one component; force skipped when g == 0 or apply_force == 0.
+__global__ void k_force_enforce(double *__restrict__ a, Dims d, int comp, double g,
+                                const DevScalars *__restrict__ sc, int apply_force,
+                                const uint8_t *__restrict__ label) {
+    Lat L = lat(d, comp);
+    int64_t n = (int64_t)L.mx * L.my * L.mz;
+    double inc = (apply_force && g != 0.0) ? g * sc->dt : 0.0;
+    for (int64_t f = gtid(); f < n; f += gstride()) {
+        int i = (int)(f % L.mx), j = (int)((f / L.mx) % L.my), k = (int)(f / ((int64_t)L.mx * L.my));
+        int64_t lo, hi;
+        bool solid = !face_cells(d, comp, i, j, k, lo, hi) || label[lo] == SOLID || label[hi] == SOLID;
+        if (solid) a[f] = 0.0;
+        else if (apply_force && g != 0.0) a[f] = a[f] + inc;
+    }
+}
+
+void stage_force(Ctx &c, const flip_step_params &prm) {
+    double *arr[3] = {c.u, c.v, c.w};
+    int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
+    for (int comp = 0; comp < 3; comp++) {
+        k_force_enforce<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(arr[comp], c.d, comp,
+                                                                  prm.gravity[comp], c.sc, 1,
+                                                                  c.label);
+        c.launches++;
+    }
+}
+
+void launch_enforce(Ctx &c, double *u, double *v, double *w) {
+    double *arr[3] = {u, v, w};
+    int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
+    for (int comp = 0; comp < 3; comp++) {
+        k_force_enforce<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(arr[comp], c.d, comp, 0.0, c.sc,
+                                                                  0, c.label);
+        c.launches++;
+    }
+}
+
+// apply_pressure_gradient (pressure.py:343-380): scale = dt / (rho*dtau).
+__global__ void k_gradient(double *__restrict__ a, Dims d, int comp, const double *__restrict__ p,
+                           const uint8_t *__restrict__ label, const DevScalars *__restrict__ sc,
+                           double rho_dtau) {
+    Lat L = lat(d, comp);
+    int64_t n = (int64_t)L.mx * L.my * L.mz;
+    double scale = sc->dt / rho_dtau;
+    for (int64_t f = gtid(); f < n; f += gstride()) {
+        int i = (int)(f % L.mx), j = (int)((f / L.mx) % L.my), k = (int)(f / ((int64_t)L.mx * L.my));
+        int64_t lo, hi;
+        if (!face_cells(d, comp, i, j, k, lo, hi)) {
+            a[f] = 0.0;
+            continue;
+        }
+        uint8_t la = label[lo], lb = label[hi];
+        if (la == SOLID || lb == SOLID) a[f] = 0.0;
+        else if (la == FLUID || lb == FLUID) a[f] = a[f] - scale * (p[hi] - p[lo]);
+    }
+}
+
+// One synchronous extrapolation layer (grid.py:231-263) on two arrays that
+// share masks (grid and grid_old, sim.py:276-279).  Reads values only where
+// kin is set and writes only where it is not, so the update is in place.
+// Accumulation order: 0 + v(k+1) + v(k-1) + v(j+1) + v(j-1) + v(i+1) + v(i-1).
+__global__ void k_extrap_layer(double *__restrict__ A, double *__restrict__ B, Lat L,
+                               const uint8_t *__restrict__ kin, uint8_t *__restrict__ kout) {
+    int64_t n = (int64_t)L.mx * L.my * L.mz, sy = L.mx, sz = (int64_t)L.mx * L.my;
+    for (int64_t f = gtid(); f < n; f += gstride()) {
+        if (kin[f]) {
+            kout[f] = 1;
+            continue;
+        }
+        int i = (int)(f % L.mx), j = (int)((f / L.mx) % L.my), k = (int)(f / sz);
+        int64_t nb[6] = {f + sz, f - sz, f + sy, f - sy, f + 1, f - 1};
+        bool ok[6] = {k + 1 < L.mz, k >= 1, j + 1 < L.my, j >= 1, i + 1 < L.mx, i >= 1};
+        double a = 0.0, b = 0.0;
+        int cnt = 0;
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+            bool kn = ok[q] && kin[nb[q]];
+            cnt += kn;
+            a = a + (kn ? A[nb[q]] : 0.0);
+            if (B) b = b + (kn ? B[nb[q]] : 0.0);
+        }
+        if (cnt > 0) {
+            A[f] = a / (double)cnt;
+            if (B) B[f] = b / (double)cnt;
+            kout[f] = 1;
+        } else {
+            kout[f] = 0;
+        }
+    }
+}
+
+// pressure_field (pressure.py:49-53) is written by stage_project.
+void stage_apply_gradient(Ctx &c, const flip_step_params &prm) {
+    double *g[3] = {c.u, c.v, c.w}, *o[3] = {c.uo, c.vo, c.wo};
+    uint8_t *k0[3] = {c.ku, c.kv, c.kw}, *k1[3] = {c.ku1, c.kv1, c.kw1};
+    int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
+    // scratch mask pairs: layer l reads (l == 0 ? P2G mask : s[(l-1)&1]), writes s[l&1]
+    uint8_t *s0[3] = {c.ku1, c.kv1, c.kw1};
+    uint8_t *s1[3] = {c.ku1 + c.nfu, c.kv1 + c.nfv, c.kw1 + c.nfw};
+    (void)k1;
+    for (int comp = 0; comp < 3; comp++) {
+        k_gradient<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(g[comp], c.d, comp, c.p, c.label, c.sc,
+                                                             prm.rho_dtau_h);
+        c.launches++;
+    }
+    for (int comp = 0; comp < 3; comp++) {
+        Lat L = lat(c.d, comp);
+        for (int l = 0; l < prm.extrapolation_layers; l++) {
+            const uint8_t *kin = l == 0 ? k0[comp] : ((l - 1) & 1 ? s1[comp] : s0[comp]);
+            uint8_t *kout = (l & 1) ? s1[comp] : s0[comp];
+            k_extrap_layer<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(g[comp], o[comp], L, kin, kout);
+            c.launches++;
+        }
+    }
+    launch_enforce(c, c.u, c.v, c.w);
+}
+
+// divergence_field (grid.py:147-156)
+__global__ void k_divergence(Dims d, const double *__restrict__ u, const double *__restrict__ v,
+                             const double *__restrict__ w, double *__restrict__ div) {
+    int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        int64_t fu = i + (int64_t)j * (d.nx + 1) + k * (int64_t)(d.nx + 1) * d.ny;
+        int64_t fv = i + (int64_t)j * d.nx + k * (int64_t)d.nx * (d.ny + 1);
+        int64_t fw = c;
+        div[c] = (((((u[fu + 1] - u[fu]) + v[fv + d.nx]) - v[fv]) + w[fw + sxy]) - w[fw]) / d.dtau;
+    }
+}
+
+void launch_divergence(Ctx &c, double *div_dev) {
+    k_divergence<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.d, c.u, c.v, c.w, div_dev);
+    c.launches++;
+}
+
+}  // namespace flip

@@ -1,0 +1,136 @@
+// ops.cuh — device context and kernel launcher declarations for libflipb200.
+#pragma once
+#include <string>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace flip {
+
+struct ParticlePtrs {
+    double *a[6];  // pos_x, pos_y, pos_z, vel_x, vel_y, vel_z (particles.py:23-28)
+};
+
+// Device-resident scalars of one step (one struct, read back once per step).
+struct DevScalars {
+    double dt;
+    unsigned long long s2max_bits;      // compute_dt max |v|^2
+    int box_min[3], box_max[3];         // interior_box (grid.py:121-132)
+    double lo[3], hi[3];
+    int n_particles;                    // count entering the stage
+    int nrows, npinned;
+    int total;                          // scratch total for scans
+    unsigned long long rhsmax_bits;     // max |rhs|
+    unsigned long long res_bits;        // max |r| or max residual
+    double target, res, sigma, sigma_new, curv, alpha, beta;
+    int iter, done, converged, status;  // solver loop state
+    long long err_cell, err_it;
+    double err_value;
+    int reseed_changed, new_total;
+    int nlevels;
+    int pad;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    Dims d{};
+    int64_t ncells = 0, nfu = 0, nfv = 0, nfw = 0;
+    int64_t cap = 0;        // particle capacity
+    int64_t n = 0;          // particle count (host mirror)
+    ParticlePtrs P{}, Q{};  // current and back particle buffers
+    double *u = nullptr, *v = nullptr, *w = nullptr, *p = nullptr;
+    uint8_t *label = nullptr;
+    double *uo = nullptr, *vo = nullptr, *wo = nullptr;
+    uint8_t *ku = nullptr, *kv = nullptr, *kw = nullptr, *ku1 = nullptr, *kv1 = nullptr,
+            *kw1 = nullptr;
+    int *count = nullptr, *offset = nullptr;  // offset has ncells + 1 entries
+    int *count2 = nullptr, *offset2 = nullptr, *nadd = nullptr;  // reseed output hash
+    int *keys0 = nullptr, *keys1 = nullptr, *vals0 = nullptr, *vals1 = nullptr;
+    int *keys_sorted = nullptr;  // cell of each binned particle (valid after BIN)
+    int *hist = nullptr;
+    int *scan_tmp = nullptr;
+    // pressure system (rows = unpinned FLUID cells ascending, pressure.py:76-166)
+    int *rowscan = nullptr;      // exclusive scan of isrow over cells
+    uint8_t *isrow = nullptr;
+    int *parent = nullptr;       // union-find over FLUID cells
+    uint8_t *has_air = nullptr;
+    int *cell_of_row = nullptr;
+    int *nbr = nullptr;          // [6][ncells] neighbour rows, -1 = none
+    double *diagd = nullptr;     // non-SOLID neighbour count (float64 like the reference)
+    double *rhs = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *s = nullptr, *q = nullptr,
+           *tq = nullptr, *precon = nullptr, *xtmp = nullptr;
+    unsigned long long *u64_scratch = nullptr;
+    int *lvl = nullptr, *lvl_rows = nullptr, *lvl_off = nullptr, *lvl_cnt = nullptr;
+    double *dot_part = nullptr;
+    DevScalars *sc = nullptr;    // device
+    DevScalars *sch = nullptr;   // pinned host mirror
+    cudaEvent_t ev[FLIP_NSTAGES + 1]{};
+    int64_t launches = 0;
+    int known_valid = 0;
+    int keys_valid = 0;   // keys_sorted matches the current binned particles
+};
+
+// ---- sort / scan ----
+__global__ void k_iota(int *a, int64_t n);
+__global__ void k_gather6(ParticlePtrs src, ParticlePtrs dst, const int *__restrict__ perm,
+                          int64_t n);
+int64_t radix_hist_ints(int64_t cap, int64_t ncells);
+int radix_sort_cells(int *k0, int *k1, int *v0, int *v1, int64_t n, int64_t ncells, int *hist,
+                     int *scan_tmp, int *scan_total, cudaStream_t st, int **keys_sorted,
+                     int **perm_out, int64_t *launches);
+
+// ---- stage launchers (ctx-based, stream-ordered, no host sync) ----
+void stage_dt(Ctx &c, const flip_step_params &prm);
+void stage_advect(Ctx &c, const flip_step_params &prm);
+void stage_bin(Ctx &c);                                // keys + count + scan + sort + gather
+void stage_bin_from_keys(Ctx &c);                      // same, keys/count already computed
+void stage_classify(Ctx &c);
+void stage_p2g(Ctx &c, const flip_step_params &prm);   // + grid_old copy, known masks
+void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force);
+void stage_force(Ctx &c, const flip_step_params &prm); // body force + enforce
+int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep);  // syncs
+void stage_apply_gradient(Ctx &c, const flip_step_params &prm);
+void stage_g2p(Ctx &c, const flip_step_params &prm);
+void stage_reseed(Ctx &c, const flip_step_params &prm);
+
+void launch_set_solid_shell(Ctx &c);
+int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed);
+void launch_divergence(Ctx &c, double *div_dev);
+void launch_enforce(Ctx &c, double *u, double *v, double *w);
+
+// ---- kernel-level helpers shared with the plugin API ----
+void launch_sample_many(const Dims &d, const double *u, const double *v, const double *w,
+                        int64_t n, const double *px, const double *py, const double *pz,
+                        double *vx, double *vy, double *vz, cudaStream_t st);
+void launch_p2g_component(const Dims &d, int comp, const double *vel, const double *px,
+                          const double *py, const double *pz, const int *offset,
+                          const int *count, double *out, double *den, cudaStream_t st);
+
+// pairwise (numpy) dot: result written to *out_dev; tmp holds >= dot_tmp_doubles(n)
+int64_t dot_tmp_doubles(int64_t n);
+void launch_pairwise_dot(const double *a, const double *b, int64_t n, double *tmp,
+                         double *out_dev, cudaStream_t st, int64_t *launches);
+
+inline unsigned nblocks(int64_t n, int threads = kThreads, int64_t cap = 148 * 32) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (unsigned)b;
+}
+
+// Dims from grid size; pow2 flags dtau == 2^-k exactly.
+Dims make_dims(int64_t nx, int64_t ny, int64_t nz, double dtau, const double origin[3]);
+
+void set_error(const std::string &msg);
+
+#define FLIP_CUDA_OK(expr)                                                                 \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            ::flip::set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));         \
+            return FLIP_E_CUDA;                                                            \
+        }                                                                                  \
+    } while (0)
+
+}  // namespace flip

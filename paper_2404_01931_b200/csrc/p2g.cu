@@ -1,0 +1,155 @@
+// p2g.cu — particle-to-grid transfer as a deterministic per-face gather
+// (flipsim/transfer.py:35-57 -> _kernels/_core.pyx:93-176), no atomics.
+//
+// Each thread owns one face of one component lattice and accumulates, with
+// Kahan compensation, w*v and w over the particles of its candidate cells in
+// the reference's order (cells z-outer, y, x-inner; particles in hash order).
+// Because particles are cell-sorted, the candidate cells of one (y,z) row are
+// one contiguous particle range [offset[first], offset[last+1]), so a face
+// walks at most 9 contiguous ranges.  The epilogue fuses
+// grid_old.copy_velocities_from (grid.py:104-107), the known mask
+// (weights > 0, transfer.py:53), add_body_force (grid.py:193-202) and
+// enforce_solid_boundaries (grid.py:219-228).
+#include "ops.cuh"
+
+namespace flip {
+
+struct FaceLattice {
+    int fnx, fny, fnz;
+    double offx, offy, offz;
+};
+
+__host__ __device__ inline FaceLattice lattice(const Dims &d, int comp) {
+    if (comp == 0) return {d.nx + 1, d.ny, d.nz, 0.0, 0.5, 0.5};
+    if (comp == 1) return {d.nx, d.ny + 1, d.nz, 0.5, 0.0, 0.5};
+    return {d.nx, d.ny, d.nz + 1, 0.5, 0.5, 0.0};
+}
+
+// Face touches SOLID or lies on the domain boundary (grid.py:205-216).
+__device__ __forceinline__ bool face_solid(const Dims &d, const uint8_t *__restrict__ label,
+                                           int comp, int fi, int fj, int fk) {
+    int64_t sxy = (int64_t)d.nx * d.ny;
+    if (comp == 0) {
+        if (fi == 0 || fi == d.nx) return true;
+        int64_t hi = fi + (int64_t)fj * d.nx + fk * sxy;
+        return label[hi - 1] == SOLID || label[hi] == SOLID;
+    }
+    if (comp == 1) {
+        if (fj == 0 || fj == d.ny) return true;
+        int64_t hi = fi + (int64_t)fj * d.nx + fk * sxy;
+        return label[hi - d.nx] == SOLID || label[hi] == SOLID;
+    }
+    if (fk == 0 || fk == d.nz) return true;
+    int64_t hi = fi + (int64_t)fj * d.nx + fk * sxy;
+    return label[hi - sxy] == SOLID || label[hi] == SOLID;
+}
+
+struct P2GOut {
+    double *grid;     // value (+ force, walls zeroed when fuse_force)
+    double *old;      // raw value (grid_old), may be null
+    uint8_t *known;   // weights > 0, may be null
+    double *den;      // raw weights, may be null
+};
+
+// CONTIG: offset has ncells+1 entries and segments are back to back (a hash
+// from bin_particles).  !CONTIG: generic (offset, count) pairs per cell like
+// the Cython signature, used by the plugin API.
+template <bool CONTIG>
+__global__ void __launch_bounds__(kThreads)
+k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict__ py,
+      const double *__restrict__ pz, const double *__restrict__ vel,
+      const int *__restrict__ offset, const int *__restrict__ count, P2GOut out,
+      const uint8_t *__restrict__ label, const DevScalars *__restrict__ sc, double g,
+      int fuse_force) {
+    FaceLattice L = lattice(d, comp);
+    int64_t nf = (int64_t)L.fnx * L.fny * L.fnz;
+    int nx = d.nx, ny = d.ny, nz = d.nz;
+    int64_t sxy = (int64_t)nx * ny;
+    double gdt = 0.0;
+    if (fuse_force && g != 0.0) gdt = g * sc->dt;
+    for (int64_t f = gtid(); f < nf; f += gstride()) {
+        int fi = (int)(f % L.fnx);
+        int fj = (int)((f / L.fnx) % L.fny);
+        int fk = (int)(f / ((int64_t)L.fnx * L.fny));
+        double fpx = d.ox + ((double)fi + L.offx) * d.dtau;
+        double fpy = d.oy + ((double)fj + L.offy) * d.dtau;
+        double fpz = d.oz + ((double)fk + L.offz) * d.dtau;
+        int cxlo = max(fi - 1, 0), cxhi = min(comp == 0 ? fi : fi + 1, nx - 1);
+        int cylo = max(fj - 1, 0), cyhi = min(comp == 1 ? fj : fj + 1, ny - 1);
+        int czlo = max(fk - 1, 0), czhi = min(comp == 2 ? fk : fk + 1, nz - 1);
+        double num = 0.0, dsum = 0.0, cn = 0.0, cd = 0.0;
+        for (int cz = czlo; cz <= czhi; cz++) {
+            for (int cy = cylo; cy <= cyhi; cy++) {
+                int64_t row = (int64_t)cy * nx + cz * sxy;
+                int nseg = CONTIG ? 1 : cxhi - cxlo + 1;
+                for (int sgi = 0; sgi < nseg; sgi++) {
+                    int t0, t1;
+                    if (CONTIG) {
+                        t0 = __ldg(offset + row + cxlo);
+                        t1 = __ldg(offset + row + cxhi + 1);
+                    } else {
+                        int64_t cell = row + cxlo + sgi;
+                        t0 = __ldg(offset + cell);
+                        t1 = t0 + __ldg(count + cell);
+                    }
+                    for (int t = t0; t < t1; t++) {
+                        double hx = hat(div_dtau(d, __ldg(px + t) - fpx));
+                        if (hx == 0.0) continue;  // w = 0 regardless of hy, hz
+                        double hy = hat(div_dtau(d, __ldg(py + t) - fpy));
+                        double hz = hat(div_dtau(d, __ldg(pz + t) - fpz));
+                        double wgt = (hx * hy) * hz;
+                        if (wgt > 0.0) {
+                            double yk = wgt * __ldg(vel + t) - cn;
+                            double tk = num + yk;
+                            cn = (tk - num) - yk;
+                            num = tk;
+                            yk = wgt - cd;
+                            tk = dsum + yk;
+                            cd = (tk - dsum) - yk;
+                            dsum = tk;
+                        }
+                    }
+                }
+            }
+        }
+        double val = dsum > 0.0 ? num / dsum : 0.0;
+        if (out.den) out.den[f] = dsum;
+        if (out.old) out.old[f] = val;
+        if (out.known) out.known[f] = dsum > 0.0;
+        double gv = val;
+        if (fuse_force) {
+            if (g != 0.0) gv = val + gdt;
+            if (face_solid(d, label, comp, fi, fj, fk)) gv = 0.0;
+        }
+        out.grid[f] = gv;
+    }
+}
+
+void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force) {
+    double *grid[3] = {c.u, c.v, c.w}, *old[3] = {c.uo, c.vo, c.wo};
+    uint8_t *known[3] = {c.ku, c.kv, c.kw};
+    int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
+    for (int comp = 0; comp < 3; comp++) {
+        P2GOut o{grid[comp], old[comp], known[comp], nullptr};
+        double g = prm ? prm->gravity[comp] : 0.0;
+        k_p2g<true><<<nblocks(nf[comp], kThreads, (int64_t)1 << 30), kThreads, 0, c.st>>>(
+            c.d, comp, c.P.a[0], c.P.a[1], c.P.a[2], c.P.a[3 + comp], c.offset, nullptr, o,
+            c.label, c.sc, g, fuse_force);
+        c.launches++;
+    }
+    c.known_valid = 1;
+}
+
+void stage_p2g(Ctx &c, const flip_step_params &prm) { stage_p2g_impl(c, &prm, 0); }
+
+void launch_p2g_component(const Dims &d, int comp, const double *vel, const double *px,
+                          const double *py, const double *pz, const int *offset,
+                          const int *count, double *out, double *den, cudaStream_t st) {
+    FaceLattice L = lattice(d, comp);
+    int64_t nf = (int64_t)L.fnx * L.fny * L.fnz;
+    P2GOut o{out, nullptr, nullptr, den};
+    k_p2g<false><<<nblocks(nf, kThreads, (int64_t)1 << 30), kThreads, 0, st>>>(
+        d, comp, px, py, pz, vel, offset, count, o, nullptr, nullptr, 0.0, 0);
+}
+
+}  // namespace flip

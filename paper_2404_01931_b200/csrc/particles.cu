@@ -1,0 +1,395 @@
+// particles.cu — particle-side stages: CFL dt, advection fused with the cell
+// key + histogram, binning, classification, G2P, reseeding and scene seeding.
+// Each kernel cites the reference function it re-implements; arithmetic is
+// written in the reference's association order (see common.cuh).
+#include "ops.cuh"
+
+namespace flip {
+
+// ------------------------------------------------------------ compute_dt --
+// flipsim/particles.py:214-224.  max is order-free -> atomicMax on bits.
+__global__ void k_maxv2(ParticlePtrs P, int64_t n, unsigned long long *out) {
+    double m = 0.0;
+    for (int64_t t = gtid(); t < n; t += gstride()) {
+        double vx = P.a[3][t], vy = P.a[4][t], vz = P.a[5][t];
+        double s2 = ((vx * vx) + (vy * vy)) + (vz * vz);
+        m = fmax(m, s2);
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(out, m);
+}
+
+__global__ void k_dt_final(DevScalars *sc, double alpha_dtau, double dt_max) {
+    double s_max = sqrt(__longlong_as_double((long long)sc->s2max_bits));
+    double dt = dt_max;
+    if (s_max != 0.0) {
+        double cand = alpha_dtau / s_max;
+        dt = cand < dt_max ? cand : dt_max;
+    }
+    sc->dt = dt;
+}
+
+void stage_dt(Ctx &c, const flip_step_params &prm) {
+    cudaMemsetAsync(&c.sc->s2max_bits, 0, sizeof(unsigned long long), c.st);
+    if (c.n > 0) {
+        k_maxv2<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, &c.sc->s2max_bits);
+        c.launches++;
+    }
+    k_dt_final<<<1, 1, 0, c.st>>>(c.sc, prm.alpha_dtau_h, prm.dt_max);
+    c.launches++;
+}
+
+// ---------------------------------------------------------------- advect --
+// interior_box (flipsim/grid.py:121-132): bounding box of non-SOLID cells.
+__global__ void k_box_reset(DevScalars *sc) {
+    for (int a = 0; a < 3; a++) {
+        sc->box_min[a] = 0x7fffffff;
+        sc->box_max[a] = -1;
+    }
+}
+
+__global__ void k_box_reduce(const uint8_t *__restrict__ label, Dims d, DevScalars *sc) {
+    int64_t nc = d.ncells();
+    int mn[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, mx[3] = {-1, -1, -1};
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        if (label[c] == SOLID) continue;
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((int64_t)d.nx * d.ny));
+        mn[0] = min(mn[0], i); mx[0] = max(mx[0], i);
+        mn[1] = min(mn[1], j); mx[1] = max(mx[1], j);
+        mn[2] = min(mn[2], k); mx[2] = max(mx[2], k);
+    }
+    for (int a = 0; a < 3; a++) {
+        for (int o = 16; o; o >>= 1) {
+            mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+        if ((threadIdx.x & 31) == 0 && mx[a] >= 0) {
+            atomicMin(&sc->box_min[a], mn[a]);
+            atomicMax(&sc->box_max[a], mx[a]);
+        }
+    }
+}
+
+__global__ void k_box_final(Dims d, DevScalars *sc) {
+    double o[3] = {d.ox, d.oy, d.oz};
+    for (int a = 0; a < 3; a++) {
+        sc->lo[a] = o[a] + (double)sc->box_min[a] * d.dtau;
+        sc->hi[a] = o[a] + (double)(sc->box_max[a] + 1) * d.dtau;
+    }
+}
+
+// flipsim/particles.py:227-248 (forward Euler + per-axis clamp), fused with
+// cell_index_many (binning.py:37-42) and the per-cell count (binning.py:90).
+__global__ void k_advect_key(ParticlePtrs P, int64_t n, const DevScalars *__restrict__ sc,
+                             double skin, Dims d, int *__restrict__ keys, int *__restrict__ count) {
+    double dt = sc->dt;
+    double lo[3] = {sc->lo[0], sc->lo[1], sc->lo[2]}, hi[3] = {sc->hi[0], sc->hi[1], sc->hi[2]};
+    for (int64_t t = gtid(); t < n; t += gstride()) {
+        double pos[3];
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            double q = P.a[a][t] + (P.a[3 + a][t] * dt);
+            if (q <= lo[a]) q = lo[a] + skin;
+            else if (q >= hi[a]) q = hi[a] - skin;
+            P.a[a][t] = q;
+            pos[a] = q;
+        }
+        int cell = cell_of(d, pos[0], pos[1], pos[2]);
+        keys[t] = cell;
+        atomicAdd(&count[cell], 1);
+    }
+}
+
+void stage_advect(Ctx &c, const flip_step_params &prm) {
+    k_box_reset<<<1, 1, 0, c.st>>>(c.sc);
+    k_box_reduce<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.d, c.sc);
+    k_box_final<<<1, 1, 0, c.st>>>(c.d, c.sc);
+    cudaMemsetAsync(c.count, 0, sizeof(int) * c.ncells, c.st);
+    c.launches += 3;
+    if (c.n > 0) {
+        k_advect_key<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.sc, prm.skin_h, c.d, c.keys0,
+                                                          c.count);
+        c.launches++;
+    }
+}
+
+// ------------------------------------------------------------------- bin --
+// cell_index_many + bincount (binning.py:88-90) when advect did not run.
+__global__ void k_keys_count(ParticlePtrs P, int64_t n, Dims d, int *__restrict__ keys,
+                             int *__restrict__ count) {
+    for (int64_t t = gtid(); t < n; t += gstride()) {
+        int cell = cell_of(d, P.a[0][t], P.a[1][t], P.a[2][t]);
+        keys[t] = cell;
+        atomicAdd(&count[cell], 1);
+    }
+}
+
+void stage_bin_from_keys(Ctx &c) {
+    // offset = exclusive_scan(count) (binning.py:91); offset[ncells] = N
+    exclusive_scan(ArrayIn{c.count}, c.ncells, c.offset, c.offset + c.ncells, c.scan_tmp, c.st);
+    c.launches += 3;
+    int *perm = nullptr;
+    radix_sort_cells(c.keys0, c.keys1, c.vals0, c.vals1, c.n, c.ncells, c.hist, c.scan_tmp,
+                     &c.sc->total, c.st, &c.keys_sorted, &perm, &c.launches);
+    if (c.n > 0) {
+        k_gather6<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.Q, perm, c.n);
+        c.launches++;
+        std::swap(c.P, c.Q);
+    }
+    c.keys_valid = 1;
+}
+
+void stage_bin(Ctx &c) {
+    cudaMemsetAsync(c.count, 0, sizeof(int) * c.ncells, c.st);
+    if (c.n > 0) {
+        k_keys_count<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.d, c.keys0, c.count);
+        c.launches++;
+    }
+    stage_bin_from_keys(c);
+}
+
+// -------------------------------------------------------------- classify --
+// flipsim/grid.py:185-190
+__global__ void k_classify(uint8_t *__restrict__ label, const int *__restrict__ count, int64_t nc) {
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        uint8_t l = label[c];
+        if (l != SOLID) label[c] = count[c] > 0 ? FLUID : AIR;
+    }
+}
+
+void stage_classify(Ctx &c) {
+    k_classify<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.count, c.ncells);
+    c.launches++;
+}
+
+// ------------------------------------------------------------------- G2P --
+// flipsim/transfer.py:60-82 with sample_velocity_many (_core.pyx:68-90).
+__global__ void k_g2p(ParticlePtrs P, int64_t n, Dims d, const double *__restrict__ un,
+                      const double *__restrict__ vn, const double *__restrict__ wn,
+                      const double *__restrict__ uo, const double *__restrict__ vo,
+                      const double *__restrict__ wo, double f) {
+    for (int64_t t = gtid(); t < n; t += gstride()) {
+        double px = P.a[0][t], py = P.a[1][t], pz = P.a[2][t];
+        double ax, ay, az;
+        sample_vel(d, un, vn, wn, px, py, pz, ax, ay, az);
+        if (f == 0.0) {
+            P.a[3][t] = ax;
+            P.a[4][t] = ay;
+            P.a[5][t] = az;
+            continue;
+        }
+        double bx, by, bz;
+        sample_vel(d, uo, vo, wo, px, py, pz, bx, by, bz);
+        double g = 1.0 - f;
+        P.a[3][t] = g * ax + f * ((P.a[3][t] + ax) - bx);
+        P.a[4][t] = g * ay + f * ((P.a[4][t] + ay) - by);
+        P.a[5][t] = g * az + f * ((P.a[5][t] + az) - bz);
+    }
+}
+
+void stage_g2p(Ctx &c, const flip_step_params &prm) {
+    if (c.n == 0) return;
+    k_g2p<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.d, c.u, c.v, c.w, c.uo, c.vo, c.wo,
+                                               prm.flip_fraction);
+    c.launches++;
+}
+
+__global__ void k_sample_many(Dims d, const double *__restrict__ u, const double *__restrict__ v,
+                              const double *__restrict__ w, int64_t n, const double *px,
+                              const double *py, const double *pz, double *vx, double *vy,
+                              double *vz) {
+    for (int64_t t = gtid(); t < n; t += gstride())
+        sample_vel(d, u, v, w, px[t], py[t], pz[t], vx[t], vy[t], vz[t]);
+}
+
+void launch_sample_many(const Dims &d, const double *u, const double *v, const double *w,
+                        int64_t n, const double *px, const double *py, const double *pz,
+                        double *vx, double *vy, double *vz, cudaStream_t st) {
+    if (n <= 0) return;
+    k_sample_many<<<nblocks(n), kThreads, 0, st>>>(d, u, v, w, n, px, py, pz, vx, vy, vz);
+}
+
+// ---------------------------------------------------------------- reseed --
+// flipsim/particles.py:157-178: per-cell refill/cull counts.
+__global__ void k_reseed_count(const int *__restrict__ count, const uint8_t *__restrict__ label,
+                               int64_t nc, int density, int *__restrict__ nadd,
+                               int *__restrict__ new_count, DevScalars *sc) {
+    int target = density * density * density;
+    if (target > MAX_PER_CELL) target = MAX_PER_CELL;
+    int changed = 0;
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        int cnt = count[c];
+        int add = 0;
+        if (label[c] == FLUID && cnt < MIN_PER_CELL) add = target - cnt > 0 ? target - cnt : 0;
+        nadd[c] = add;
+        new_count[c] = (cnt < MAX_PER_CELL ? cnt : MAX_PER_CELL) + add;
+        changed |= (add > 0) | (cnt > MAX_PER_CELL);
+    }
+    changed = __any_sync(0xffffffffu, changed);
+    if (changed && (threadIdx.x & 31) == 0) sc->reseed_changed = 1;
+}
+
+// cells_of = np.repeat(arange(ncells), count) (particles.py:183)
+__global__ void k_cells_from_hash(const int *__restrict__ offset, int64_t nc, int *__restrict__ cellp) {
+    for (int64_t c = gtid(); c < nc; c += gstride())
+        for (int t = offset[c]; t < offset[c + 1]; t++) cellp[t] = (int)c;
+}
+
+// Survivors keep their within-cell index (particles.py:180-189).
+__global__ void k_reseed_copy(ParticlePtrs P, ParticlePtrs Q, int64_t n,
+                              const int *__restrict__ cell_of_p, const int *__restrict__ offset,
+                              const int *__restrict__ new_offset, const DevScalars *sc) {
+    if (!sc->reseed_changed) return;
+    for (int64_t t = gtid(); t < n; t += gstride()) {
+        int c = cell_of_p[t];
+        int within = (int)t - offset[c];
+        if (within >= MAX_PER_CELL) continue;
+        int64_t dst = (int64_t)new_offset[c] + within;
+#pragma unroll
+        for (int a = 0; a < 6; a++) Q.a[a][dst] = P.a[a][t];
+    }
+}
+
+// New particles in the first free subcells, velocity sampled from the grid
+// (particles.py:190-206).
+__global__ void k_reseed_emit(ParticlePtrs Q, Dims d, const int *__restrict__ count,
+                              const int *__restrict__ nadd, const int *__restrict__ new_offset,
+                              int density, uint64_t seed, const double *__restrict__ u,
+                              const double *__restrict__ v, const double *__restrict__ w,
+                              const DevScalars *sc) {
+    if (!sc->reseed_changed) return;
+    int64_t nc = d.ncells();
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        int add = nadd[c];
+        if (add == 0) continue;
+        int cnt = count[c];
+        int64_t base = (int64_t)new_offset[c] + cnt;  // cnt < 3 <= MAX_PER_CELL
+        for (int j = 0; j < add; j++) {
+            double px, py, pz, vx, vy, vz;
+            jitter_pos(d, c, cnt + j, density, seed, px, py, pz);
+            sample_vel(d, u, v, w, px, py, pz, vx, vy, vz);
+            int64_t at = base + j;
+            Q.a[0][at] = px;
+            Q.a[1][at] = py;
+            Q.a[2][at] = pz;
+            Q.a[3][at] = vx;
+            Q.a[4][at] = vy;
+            Q.a[5][at] = vz;
+        }
+    }
+}
+
+void stage_reseed(Ctx &c, const flip_step_params &prm) {
+    int *new_count = c.count2, *new_offset = c.offset2, *nadd = c.nadd;
+    if (!c.keys_valid && c.n > 0) {  // cell of each binned particle from the hash
+        k_cells_from_hash<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.offset, c.ncells, c.keys0);
+        c.keys_sorted = c.keys0;
+        c.keys_valid = 1;
+        c.launches++;
+    }
+    cudaMemsetAsync(&c.sc->reseed_changed, 0, sizeof(int), c.st);
+    k_reseed_count<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.count, c.label, c.ncells,
+                                                             prm.density, nadd, new_count, c.sc);
+    exclusive_scan(ArrayIn{new_count}, c.ncells, new_offset, new_offset + c.ncells, c.scan_tmp,
+                   c.st);
+    c.launches += 4;
+    if (c.n > 0) {
+        k_reseed_copy<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.Q, c.n, c.keys_sorted, c.offset,
+                                                           new_offset, c.sc);
+        c.launches++;
+    }
+    k_reseed_emit<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.Q, c.d, c.count, nadd, new_offset,
+                                                            prm.density, prm.reseed_seed, c.u, c.v,
+                                                            c.w, c.sc);
+    c.launches++;
+    // the host swaps P<->Q and the hash buffers after reading reseed_changed
+}
+
+// --------------------------------------------------------------- seeding --
+// set_solid_shell (flipsim/grid.py:110-118)
+__global__ void k_solid_shell(uint8_t *label, Dims d) {
+    int64_t nc = d.ncells();
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((int64_t)d.nx * d.ny));
+        if (i == 0 || j == 0 || k == 0 || i == d.nx - 1 || j == d.ny - 1 || k == d.nz - 1)
+            label[c] = SOLID;
+    }
+}
+
+void launch_set_solid_shell(Ctx &c) {
+    k_solid_shell<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.d);
+    c.launches++;
+}
+
+// covered_cells (particles.py:103-110) with SeedRegion.contains (:92-100)
+struct CoveredIn {
+    Dims d;
+    flip_region r;
+    __device__ int operator()(int64_t idx) const {
+        double cx = d.ox + ((double)(idx % d.nx) + 0.5) * d.dtau;
+        double cy = d.oy + ((double)((idx / d.nx) % d.ny) + 0.5) * d.dtau;
+        double cz = d.oz + ((double)(idx / ((int64_t)d.nx * d.ny)) + 0.5) * d.dtau;
+        if (r.kind == 0)
+            return cx >= r.a[0] && cx <= r.b[0] && cy >= r.a[1] && cy <= r.b[1] && cz >= r.a[2] &&
+                   cz <= r.b[2];
+        double dx = cx - r.a[0], dy = cy - r.a[1], dz = cz - r.a[2];
+        return ((dx * dx) + (dy * dy)) + (dz * dz) <= r.radius * r.radius;
+    }
+};
+
+__global__ void k_compact_covered(CoveredIn in, int64_t nc, const int *__restrict__ pos,
+                                  int *__restrict__ cells) {
+    for (int64_t c = gtid(); c < nc; c += gstride())
+        if (in(c)) cells[pos[c]] = (int)c;
+}
+
+// seed (particles.py:133-149): region particles are cells x subcells, zero velocity.
+__global__ void k_seed_emit(ParticlePtrs P, int64_t base, const int *__restrict__ cells, int64_t m,
+                            int density, uint64_t seed, Dims d) {
+    int nsub = density * density * density;
+    int64_t total = m * nsub;
+    for (int64_t t = gtid(); t < total; t += gstride()) {
+        int64_t ci = t / nsub;
+        int s = (int)(t - ci * nsub);
+        double px, py, pz;
+        jitter_pos(d, cells[ci], s, density, seed, px, py, pz);
+        int64_t at = base + t;
+        P.a[0][at] = px;
+        P.a[1][at] = py;
+        P.a[2][at] = pz;
+        P.a[3][at] = 0.0;
+        P.a[4][at] = 0.0;
+        P.a[5][at] = 0.0;
+    }
+}
+
+int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed) {
+    int *pos = c.lvl, *cells = c.lvl_rows;
+    for (int k = 0; k < nreg; k++) {
+        const flip_region &r = regs[k];
+        if (r.density < 1) {
+            set_error("seed density must be >= 1");
+            return FLIP_E_ARG;
+        }
+        CoveredIn in{c.d, r};
+        exclusive_scan(in, c.ncells, pos, &c.sc->total, c.scan_tmp, c.st);
+        k_compact_covered<<<nblocks(c.ncells), kThreads, 0, c.st>>>(in, c.ncells, pos, cells);
+        c.launches += 4;
+        int m = 0;
+        FLIP_CUDA_OK(cudaMemcpyAsync(&m, &c.sc->total, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
+        int64_t add = (int64_t)m * r.density * r.density * r.density;
+        if (c.n + add > c.cap) {
+            set_error("particle capacity exceeded while seeding");
+            return FLIP_E_CAPACITY;
+        }
+        if (add > 0) {
+            k_seed_emit<<<nblocks(add), kThreads, 0, c.st>>>(c.P, c.n, cells, m, r.density, seed, c.d);
+            c.launches++;
+        }
+        c.n += add;
+    }
+    return 0;
+}
+
+}  // namespace flip

@@ -1,0 +1,1237 @@
+// pressure.cu — pressure projection: assembly (flipsim/pressure.py:76-166),
+// solvers (pressure.py:200-340, _kernels/_core.pyx:196-347) and the
+// pressure field scatter (pressure.py:49-53).
+//
+// Unknowns are the unpinned FLUID cells in ascending raw order, stored as
+// compact row vectors exactly like the reference, so every per-row formula
+// and numpy's pairwise dot order carry over unchanged:
+//   * matvec / Jacobi / RBGS rows are independent gathers;
+//   * lexicographic GS and MIC(0) substitutions are wavefronts: a row only
+//     reads -x/-y/-z rows (forward) or +x/+y/+z rows (backward), so rows on one
+//     hyperplane i+j+k are independent and the sequential result is
+//     reproduced exactly, row by row;
+//   * s.q and z.r follow numpy's recursive pairwise summation tree
+//     (np.add.reduce, pressure.py:269-271), evaluated in parallel;
+//   * max-norms are order-free (atomicMax on IEEE bits).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ops.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace flip {
+
+// ================================================================ assembly
+// Union-find over 6-connected FLUID cells with the minimum raw index as the
+// root (hooks always point larger roots at smaller ones), equivalent to
+// scipy.ndimage.label + np.minimum.at (pressure.py:110-121) for the pinning.
+__device__ __forceinline__ int uf_rep(volatile int *par, int x) {
+    int cur = par[x];
+    if (cur != x) {
+        int nxt, prev = x;
+        while (cur > (nxt = par[cur])) {
+            par[prev] = nxt;
+            prev = cur;
+            cur = nxt;
+        }
+    }
+    return cur;
+}
+
+__global__ void k_uf_init(const uint8_t *__restrict__ label, int64_t nc, int *par, uint8_t *has_air) {
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        par[c] = label[c] == FLUID ? (int)c : -1;
+        has_air[c] = 0;
+    }
+}
+
+__device__ __forceinline__ void uf_unite(int *par, int a, int b) {
+    volatile int *vp = par;
+    int va = uf_rep(vp, a), vb = uf_rep(vp, b);
+    bool repeat;
+    do {
+        repeat = false;
+        if (va != vb) {
+            int ret;
+            if (va < vb) {
+                if ((ret = atomicCAS(&par[vb], vb, va)) != vb) {
+                    vb = ret;
+                    repeat = true;
+                }
+            } else {
+                if ((ret = atomicCAS(&par[va], va, vb)) != va) {
+                    va = ret;
+                    repeat = true;
+                }
+            }
+        }
+    } while (repeat);
+}
+
+__global__ void k_uf_link(const uint8_t *__restrict__ label, Dims d, int *par) {
+    int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        if (label[c] != FLUID) continue;
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        if (i > 0 && label[c - 1] == FLUID) uf_unite(par, (int)c, (int)(c - 1));
+        if (j > 0 && label[c - d.nx] == FLUID) uf_unite(par, (int)c, (int)(c - d.nx));
+        if (k > 0 && label[c - sxy] == FLUID) uf_unite(par, (int)c, (int)(c - sxy));
+    }
+}
+
+__device__ __forceinline__ uint8_t lab_at(const uint8_t *label, const Dims &d, int i, int j, int k) {
+    if (i < 0 || j < 0 || k < 0 || i >= d.nx || j >= d.ny || k >= d.nz) return SOLID;
+    return label[i + (int64_t)j * d.nx + (int64_t)k * d.nx * d.ny];
+}
+
+__global__ void k_uf_finish(const uint8_t *__restrict__ label, Dims d, int *par, uint8_t *has_air) {
+    int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        if (label[c] != FLUID) continue;
+        int root = uf_rep((volatile int *)par, (int)c);
+        par[c] = root;
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        bool air = lab_at(label, d, i - 1, j, k) == AIR || lab_at(label, d, i + 1, j, k) == AIR ||
+                   lab_at(label, d, i, j - 1, k) == AIR || lab_at(label, d, i, j + 1, k) == AIR ||
+                   lab_at(label, d, i, j, k - 1) == AIR || lab_at(label, d, i, j, k + 1) == AIR;
+        if (air) has_air[root] = 1;
+    }
+}
+
+// A FLUID cell is a row unless it is the root (lowest cell) of a component
+// with no AIR neighbour anywhere (pressure.py:114-130).
+struct IsRowIn {
+    const uint8_t *label;
+    const int *par;
+    const uint8_t *has_air;
+    __device__ int operator()(int64_t c) const {
+        if (label[c] != FLUID) return 0;
+        return !(par[c] == (int)c && !has_air[c]);
+    }
+};
+
+__global__ void k_rows_compact(IsRowIn in, int64_t nc, const int *__restrict__ rowscan,
+                               uint8_t *__restrict__ isrow, int *__restrict__ cell_of_row,
+                               DevScalars *sc) {
+    int pinned = 0;
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        int r = in(c);
+        isrow[c] = (uint8_t)r;
+        if (r) cell_of_row[rowscan[c]] = (int)c;
+        else if (in.label[c] == FLUID) pinned++;
+    }
+    if (pinned) atomicAdd(&sc->npinned, pinned);
+}
+
+// Per-row diag, neighbour rows (order -x,+x,-y,+y,-z,+z, pressure.py:25) and
+// rhs = -div with solid faces zeroed (pressure.py:144-151).
+__global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
+                                const uint8_t *__restrict__ isrow, const int *__restrict__ rowscan,
+                                const int *__restrict__ cell_of_row, const DevScalars *sc,
+                                const double *__restrict__ u, const double *__restrict__ v,
+                                const double *__restrict__ w, int *__restrict__ nbr, int64_t ldn,
+                                double *__restrict__ diag, double *__restrict__ rhs,
+                                unsigned long long *rhsmax) {
+    int n = sc->nrows;
+    int64_t sxy = (int64_t)d.nx * d.ny;
+    double m = 0.0;
+    for (int64_t r = gtid(); r < n; r += gstride()) {
+        int64_t c = cell_of_row[r];
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0}, dk[6] = {0, 0, 0, 0, -1, 1};
+        int ns = 0;
+        uint8_t nl[6];
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+            int ii = i + di[q], jj = j + dj[q], kk = k + dk[q];
+            uint8_t l = lab_at(label, d, ii, jj, kk);
+            nl[q] = l;
+            ns += l != SOLID;
+            int nb = -1;
+            if (l == FLUID) {
+                int64_t cc = ii + (int64_t)jj * d.nx + kk * sxy;
+                if (isrow[cc]) nb = rowscan[cc];
+            }
+            nbr[q * ldn + r] = nb;
+        }
+        diag[r] = (double)ns;
+        int64_t fu0 = i + (int64_t)j * (d.nx + 1) + (int64_t)k * (d.nx + 1) * d.ny;
+        int64_t fv0 = i + (int64_t)j * d.nx + (int64_t)k * d.nx * (d.ny + 1);
+        int64_t fw0 = c;
+        double u0 = nl[0] == SOLID ? 0.0 : u[fu0];
+        double u1 = nl[1] == SOLID ? 0.0 : u[fu0 + 1];
+        double v0 = nl[2] == SOLID ? 0.0 : v[fv0];
+        double v1 = nl[3] == SOLID ? 0.0 : v[fv0 + d.nx];
+        double w0 = nl[4] == SOLID ? 0.0 : w[fw0];
+        double w1 = nl[5] == SOLID ? 0.0 : w[fw0 + sxy];
+        double div = (((((u1 - u0) + v1) - v0) + w1) - w0) / d.dtau;
+        double rh = -div;
+        rhs[r] = rh;
+        m = fmax(m, fabs(rh));
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(rhsmax, m);
+}
+
+// pressure_field (pressure.py:49-53): dense p, solution on rows, 0 elsewhere.
+__global__ void k_pressure_field(double *__restrict__ p, int64_t nc, const uint8_t *__restrict__ isrow,
+                                 const int *__restrict__ rowscan, const double *__restrict__ x) {
+    for (int64_t c = gtid(); c < nc; c += gstride()) p[c] = isrow[c] ? x[rowscan[c]] : 0.0;
+}
+
+// ======================================================= pairwise dot (numpy)
+// numpy DOUBLE_pairwise_sum (loops_utils.h.src): n < 8 sequential from 0;
+// n <= 128: 8 strided accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+// then the tail sequentially; else split at n2 = n/2 - (n/2)%8 and add halves.
+__device__ __forceinline__ int64_t pw_split(int64_t n) {
+    int64_t n2 = n / 2;
+    return n2 - n2 % 8;
+}
+
+// 8 lanes (aligned group) evaluate one leaf; result valid in group lane 0.
+__device__ double pw_leaf8(const double *__restrict__ a, const double *__restrict__ b, int64_t s,
+                           int64_t len, int g) {
+    unsigned mask = 0xffu << (threadIdx.x & 24);
+    double res = 0.0;
+    if (len < 8) {
+        if (g == 0)
+            for (int64_t i = 0; i < len; i++) res += b ? a[s + i] * b[s + i] : a[s + i];
+        return res;
+    }
+    int64_t m = len - len % 8;
+    double r = b ? a[s + g] * b[s + g] : a[s + g];
+    for (int64_t i = 8; i < m; i += 8) r += b ? a[s + i + g] * b[s + i + g] : a[s + i + g];
+    r = r + __shfl_xor_sync(mask, r, 1, 8);
+    r = r + __shfl_xor_sync(mask, r, 2, 8);
+    r = r + __shfl_xor_sync(mask, r, 4, 8);
+    if (g == 0)
+        for (int64_t i = m; i < len; i++) r += b ? a[s + i] * b[s + i] : a[s + i];
+    return r;
+}
+
+// Exact recursive evaluation of a (small) subtree by one 8-lane group.
+__device__ double pw_node8(const double *__restrict__ a, const double *__restrict__ b, int64_t s,
+                           int64_t len, int g, int depth) {
+    if (len <= 128) return pw_leaf8(a, b, s, len, g);
+    int64_t n2 = pw_split(len);
+    double l = pw_node8(a, b, s, n2, g, depth + 1);
+    double r = pw_node8(a, b, s + n2, len - n2, g, depth + 1);
+    return l + r;
+}
+
+// Phase 1: the 2^cut nodes at the deepest complete level, 32 per block, then
+// a perfect-tree reduction of the block's 32 node sums (pairs 2i, 2i+1 first).
+__global__ void k_dot_nodes(const double *__restrict__ a, const double *__restrict__ b, int64_t n,
+                            int cut, double *__restrict__ out) {
+    __shared__ double sv[32];
+    int64_t nodes = (int64_t)1 << cut;
+    int64_t node = (int64_t)blockIdx.x * 32 + (threadIdx.x >> 3);
+    int g = threadIdx.x & 7;
+    double val = 0.0;
+    if (node < nodes) {
+        int64_t s = 0, len = n;
+        for (int lvl = cut - 1; lvl >= 0; lvl--) {
+            int64_t n2 = pw_split(len);
+            if ((node >> lvl) & 1) {
+                s += n2;
+                len -= n2;
+            } else {
+                len = n2;
+            }
+        }
+        val = pw_node8(a, b, s, len, g, 0);
+    }
+    if (g == 0) sv[threadIdx.x >> 3] = val;
+    __syncthreads();
+    int cnt = nodes < 32 ? (int)nodes : 32;
+    if (threadIdx.x == 0) {
+        for (int st = 1; st < cnt; st <<= 1)
+            for (int i = 0; i + st < cnt; i += 2 * st) sv[i] = sv[i] + sv[i + st];
+        out[blockIdx.x] = sv[0];
+    }
+}
+
+enum DotEpi { EPI_STORE = 0, EPI_CURV = 1, EPI_SIGMA_NEW = 2, EPI_SIGMA0 = 3 };
+
+__device__ void dot_epilogue(double v, int epi, double *out, DevScalars *sc) {
+    if (epi == EPI_STORE) {
+        *out = v;
+    } else if (epi == EPI_SIGMA0) {
+        sc->sigma = v;
+    } else if (sc->done) {
+        return;  // iteration skipped after convergence / breakdown
+    } else if (epi == EPI_CURV) {  // pressure.py:316-320
+        sc->curv = v;
+        if (v <= 0.0) {
+            sc->status = FLIP_E_BREAKDOWN;
+            sc->err_it = sc->iter + 1;
+            sc->err_value = v;
+            sc->done = 1;
+        } else {
+            sc->alpha = sc->sigma / v;
+        }
+    } else {  // EPI_SIGMA_NEW: pressure.py:328-330
+        sc->beta = v / sc->sigma;
+        sc->sigma = v;
+    }
+}
+
+// Perfect-tree reduction of cnt (power of two) values, up to 1024 per block.
+__global__ void k_dot_tree(const double *__restrict__ in, int64_t cnt, double *__restrict__ out,
+                           int epi, DevScalars *sc, double *final_out) {
+    __shared__ double sv[1024];
+    int64_t base = (int64_t)blockIdx.x * 1024;
+    int m = cnt - base < 1024 ? (int)(cnt - base) : 1024;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) sv[i] = in[base + i];
+    __syncthreads();
+    for (int st = 1; st < m; st <<= 1) {
+        for (int i = threadIdx.x * 2 * st; i + st < m; i += blockDim.x * 2 * st) sv[i] = sv[i] + sv[i + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (gridDim.x == 1) dot_epilogue(sv[0], epi, final_out, sc);
+        else out[blockIdx.x] = sv[0];
+    }
+}
+
+static int pw_cut(int64_t n) {
+    // deepest depth at which all nodes exist (all shallower nodes split)
+    std::vector<int64_t> sizes{n};
+    int cut = 0;
+    while (true) {
+        bool all_split = !sizes.empty();
+        for (int64_t s : sizes) all_split &= s > 128;
+        if (!all_split) break;
+        std::vector<int64_t> nxt;
+        for (int64_t s : sizes) {
+            int64_t n2 = s / 2 - (s / 2) % 8;
+            nxt.push_back(n2);
+            nxt.push_back(s - n2);
+        }
+        std::sort(nxt.begin(), nxt.end());
+        nxt.erase(std::unique(nxt.begin(), nxt.end()), nxt.end());
+        sizes.swap(nxt);
+        cut++;
+    }
+    return cut;
+}
+
+int64_t dot_tmp_doubles(int64_t n) {
+    int cut = pw_cut(n > 0 ? n : 1);
+    int64_t nodes = (int64_t)1 << cut;
+    return 2 * ((nodes + 31) / 32) + 64;
+}
+
+// epi/sc select a fused scalar update; for EPI_STORE the sum goes to *out_dev.
+void launch_dot(const double *a, const double *b, int64_t n, double *tmp, double *out_dev, int epi,
+                DevScalars *sc, cudaStream_t st, int64_t *launches) {
+    int cut = pw_cut(n > 0 ? n : 1);
+    int64_t nodes = (int64_t)1 << cut;
+    int64_t nb1 = (nodes + 31) / 32;
+    double *p0 = tmp, *p1 = tmp + nb1;
+    k_dot_nodes<<<(unsigned)nb1, 256, 0, st>>>(a, b, n, cut, p0);
+    (*launches)++;
+    int64_t cnt = nb1;
+    double *in = p0, *outp = p1;
+    while (true) {
+        int64_t blocks = (cnt + 1023) / 1024;
+        k_dot_tree<<<(unsigned)blocks, 256, 0, st>>>(in, cnt, outp, epi, sc, out_dev);
+        (*launches)++;
+        if (blocks == 1) break;
+        cnt = blocks;
+        std::swap(in, outp);
+    }
+}
+
+void launch_pairwise_dot(const double *a, const double *b, int64_t n, double *tmp, double *out_dev,
+                         cudaStream_t st, int64_t *launches) {
+    launch_dot(a, b, n, tmp, out_dev, EPI_STORE, nullptr, st, launches);
+}
+
+// ================================================================ solvers
+struct SysView {
+    int64_t n;
+    const int *cell;       // raw cell per row (SingularSystemError cell)
+    const int *nbr;        // [6][ldn]
+    int64_t ldn;
+    const double *diag;
+    const double *rhs;
+    double scale;          // host value, or taken from sc->... when from_dt
+};
+
+__device__ __forceinline__ double nbr_sum(const int *__restrict__ nbr, int64_t ldn, int64_t r,
+                                          const double *__restrict__ x) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 6; q++) {
+        int nb = nbr[q * ldn + r];
+        if (nb >= 0) s = s + x[nb];
+    }
+    return s;
+}
+
+// _core.pyx:196-213; optionally residual max |rhs - y| (pressure.py:59-62)
+// and copy-back of a Jacobi iterate (x <- xnew).
+__global__ void k_matvec(SysView S, const double *__restrict__ x, double *__restrict__ y,
+                         const double *__restrict__ rhs, unsigned long long *resmax,
+                         double *__restrict__ copy_to, const DevScalars *sc, int check_done) {
+    if (check_done && sc->done) return;
+    double m = 0.0;
+    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+        double s = nbr_sum(S.nbr, S.ldn, r, x);
+        double xr = x[r];
+        double yr = S.scale * (S.diag[r] * xr - s);
+        if (y) y[r] = yr;
+        if (resmax) m = fmax(m, fabs(rhs[r] - yr));
+        if (copy_to) copy_to[r] = xr;
+    }
+    if (resmax) {
+        for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(resmax, m);
+    }
+}
+
+// _core.pyx:216-234 (out of place)
+__global__ void k_jacobi(SysView S, const double *__restrict__ x, double *__restrict__ out,
+                         const DevScalars *sc, int check_done) {
+    if (check_done && sc->done) return;
+    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+        double s = nbr_sum(S.nbr, S.ldn, r, x);
+        out[r] = (S.rhs[r] / S.scale + s) / S.diag[r];
+    }
+}
+
+// _core.pyx:255-272 over an explicit row list, or over all rows of one
+// colour (parity of i+j+k of the row's cell, pressure.py:166-170).
+__global__ void k_gs_rows(SysView S, const int *__restrict__ rows, int64_t m, int color, Dims d,
+                          double *x, const DevScalars *sc, int check_done) {
+    if (check_done && sc->done) return;
+    int64_t cnt = rows ? m : S.n;
+    for (int64_t t = gtid(); t < cnt; t += gstride()) {
+        int64_t r = t;
+        if (rows) {
+            r = rows[t];
+        } else {
+            int64_t c = S.cell[r];
+            int par = (int)((c % d.nx) + (c / d.nx) % d.ny + c / ((int64_t)d.nx * d.ny)) & 1;
+            if (par != color) continue;
+        }
+        double s = nbr_sum(S.nbr, S.ldn, r, x);
+        x[r] = (S.rhs[r] / S.scale + s) / S.diag[r];
+    }
+}
+
+// ---- wavefront sweeps (level-scheduled, cooperative) ----
+enum SweepMode { SW_MIC_BUILD = 0, SW_MIC_FWD = 1, SW_MIC_BWD = 2, SW_GS = 3 };
+
+struct SweepArgs {
+    SysView S;
+    const int *lvl_rows;
+    const int *lvl_off;
+    const int *nlevels;  // device
+    int reverse;  // iterate levels in descending order
+    double tau, sigma;
+    const double *src;   // r (fwd) / q (bwd)
+    double *dst;         // q (fwd) / z (bwd) / precon (build) / x (gs)
+    const double *precon;
+    const DevScalars *sc;
+    int check_done;
+};
+
+template <int MODE>
+__device__ __forceinline__ void sweep_row(const SweepArgs &A, int r) {
+    const SysView &S = A.S;
+    const int *nb = S.nbr;
+    int64_t ld = S.ldn;
+    double sc_ = S.scale;
+    if (MODE == SW_MIC_BUILD) {  // _core.pyx:291-307
+        const int dprev[3] = {0, 2, 4}, o1[3] = {3, 1, 1}, o2[3] = {5, 5, 3};
+        double e = S.diag[r] * sc_;
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            int q = nb[dprev[p] * ld + r];
+            if (q >= 0) {
+                double pq = q < r ? A.dst[q] : 0.0;  // precon zero-initialised
+                e -= (sc_ * pq) * (sc_ * pq);
+                double others = 0.0;
+                if (nb[o1[p] * ld + q] >= 0) others -= sc_;
+                if (nb[o2[p] * ld + q] >= 0) others -= sc_;
+                e -= A.tau * (-sc_) * others * pq * pq;
+            }
+        }
+        if (e < A.sigma * S.diag[r] * sc_) e = S.diag[r] * sc_;
+        A.dst[r] = 1.0 / sqrt(e);
+    } else if (MODE == SW_MIC_FWD) {  // _core.pyx:322-332
+        double t = A.src[r];
+#pragma unroll
+        for (int q = 0; q < 6; q += 2) {
+            int k = nb[q * ld + r];
+            if (k >= 0) t += sc_ * A.precon[k] * (k < r ? A.dst[k] : 0.0);
+        }
+        A.dst[r] = t * A.precon[r];
+    } else if (MODE == SW_MIC_BWD) {  // _core.pyx:333-346
+        double t = A.src[r];
+        double pr = A.precon[r];
+#pragma unroll
+        for (int q = 1; q < 6; q += 2) {
+            int k = nb[q * ld + r];
+            if (k >= 0) t += sc_ * pr * (k > r ? A.dst[k] : 0.0);
+        }
+        A.dst[r] = t * pr;
+    } else {  // SW_GS, _core.pyx:237-252 (dst is x, in place)
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+            int k = nb[q * ld + r];
+            if (k >= 0) s += A.dst[k];
+        }
+        A.dst[r] = (S.rhs[r] / sc_ + s) / S.diag[r];
+    }
+}
+
+template <int MODE>
+__global__ void k_sweep_coop(SweepArgs A) {
+    if (A.check_done && A.sc->done) return;
+    cg::grid_group grid = cg::this_grid();
+    int nl = *A.nlevels;
+    for (int li = 0; li < nl; li++) {
+        int L = A.reverse ? nl - 1 - li : li;
+        int b = A.lvl_off[L], e = A.lvl_off[L + 1];
+        for (int64_t i = b + gtid(); i < e; i += gstride()) sweep_row<MODE>(A, A.lvl_rows[i]);
+        grid.sync();
+    }
+}
+
+// MIC(0) backward reads z of rows processed earlier; MIC forward-apply
+// needs zero-initialised q for generic (non-assembled) neighbour tables.
+
+// ---- levels ----
+// Geometric levels for assembled systems: i+j+k of the row's cell.
+__global__ void k_lvl_geom(const int *__restrict__ cell, int64_t n, Dims d, int *lvl,
+                           int *lvl_cnt) {
+    for (int64_t r = gtid(); r < n; r += gstride()) {
+        int64_t c = cell[r];
+        int L = (int)((c % d.nx) + (c / d.nx) % d.ny + c / ((int64_t)d.nx * d.ny));
+        lvl[r] = L;
+        atomicAdd(&lvl_cnt[L], 1);
+    }
+}
+
+// Generic levels by relaxation (plugin API with arbitrary nbr tables):
+//   mode 0 forward (deps: d in {0,2,4}, nb < r), 1 backward (d in {1,3,5}, nb > r,
+//   level counted from the end), 2 GS (all nb < r, plus anti-deps q < r reading r).
+__global__ void k_lvl_relax(SysView S, int mode, int *lvl, int *changed) {
+    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+        int L = lvl[r];
+        int best = L;
+        for (int q = 0; q < 6; q++) {
+            int nb = S.nbr[q * S.ldn + r];
+            if (nb < 0) continue;
+            if (mode == 0 && (q & 1) == 0 && nb < r) best = max(best, lvl[nb] + 1);
+            if (mode == 1 && (q & 1) == 1 && nb > r) best = max(best, lvl[nb] + 1);
+            if (mode == 2) {
+                if (nb < r) best = max(best, lvl[nb] + 1);
+                else if (nb > r) {  // r reads old x[nb]: nb must run after r
+                    int want = L + 1;
+                    if (lvl[nb] < want) {
+                        atomicMax(&lvl[nb], want);
+                        *changed = 1;
+                    }
+                }
+            }
+        }
+        if (best > L) {
+            atomicMax(&lvl[r], best);
+            *changed = 1;
+        }
+    }
+}
+
+__global__ void k_lvl_count(const int *lvl, int64_t n, int *lvl_cnt, int *maxlvl) {
+    int m = -1;
+    for (int64_t r = gtid(); r < n; r += gstride()) {
+        atomicAdd(&lvl_cnt[lvl[r]], 1);
+        m = max(m, lvl[r]);
+    }
+    atomicMax(maxlvl, m);
+}
+
+__global__ void k_lvl_scatter(const int *lvl, int64_t n, int *cursor, int *lvl_rows) {
+    for (int64_t r = gtid(); r < n; r += gstride()) lvl_rows[atomicAdd(&cursor[lvl[r]], 1)] = (int)r;
+}
+
+__global__ void k_copy_int(int *dst, const int *src, int64_t n) {
+    for (int64_t i = gtid(); i < n; i += gstride()) dst[i] = src[i];
+}
+
+__global__ void k_set_nlevels(DevScalars *sc, int nl) { sc->nlevels = nl; }
+__global__ void k_nlev_from_max(int *nlev) { nlev[0] = nlev[1] + 1; }
+
+// Rows bucketed by wavefront level: rows[off[L]..off[L+1]) are independent.
+struct Levels {
+    int *lvl;    // [n] level per row
+    int *cnt;    // [cap] counts, then cursors
+    int *off;    // [cap + 1]
+    int *rows;   // [n]
+    int *nlev;   // device: number of levels
+    int reverse; // sweep levels in descending order
+};
+
+// cnt must hold the per-level counts for levels [0, nlevels_max).
+static void bucket_levels(Levels &Lv, int64_t n, int nlevels_max, int *scan_tmp, cudaStream_t st,
+                          int64_t *launches) {
+    exclusive_scan(ArrayIn{Lv.cnt}, nlevels_max, Lv.off, Lv.off + nlevels_max, scan_tmp, st);
+    k_copy_int<<<nblocks(nlevels_max), kThreads, 0, st>>>(Lv.cnt, Lv.off, nlevels_max);
+    if (n > 0) k_lvl_scatter<<<nblocks(n), kThreads, 0, st>>>(Lv.lvl, n, Lv.cnt, Lv.rows);
+    *launches += 5;
+}
+
+static int coop_blocks(const void *fn) {
+    static int dev_sms = 0;
+    if (!dev_sms) {
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, 0);
+    if (per < 1) per = 1;
+    if (per > 4) per = 4;
+    return dev_sms * per;
+}
+
+template <int MODE>
+static cudaError_t launch_sweep(SweepArgs A, cudaStream_t st) {
+    static int blocks = 0;
+    if (!blocks) blocks = coop_blocks((const void *)k_sweep_coop<MODE>);
+    void *args[] = {&A};
+    return cudaLaunchCooperativeKernel((const void *)k_sweep_coop<MODE>, blocks, kThreads, args, 0, st);
+}
+
+// ---- PCG / relaxation scalar kernels ----
+__global__ void k_solve_init(DevScalars *sc, double tol, int64_t n, int relax) {
+    double rhsmax = __longlong_as_double((long long)sc->rhsmax_bits);
+    sc->target = tol * (rhsmax > 1.0 ? rhsmax : 1.0);  // pressure.py:191-193
+    sc->iter = 0;
+    sc->done = 0;
+    sc->converged = 0;
+    sc->status = 0;
+    sc->err_cell = -1;
+    sc->res_bits = 0;
+    if (relax) {
+        sc->res = INFINITY;
+    } else {
+        sc->res = rhsmax;  // r = rhs -> res = max|r| (pressure.py:306)
+        if (sc->res <= sc->target) {
+            sc->done = 1;
+            sc->converged = 1;
+        }
+    }
+    if (n == 0) {
+        sc->done = 1;
+        sc->converged = 1;
+        sc->res = 0.0;
+    }
+}
+
+__global__ void k_check_diag(SysView S, DevScalars *sc, unsigned long long *first_bad) {
+    for (int64_t r = gtid(); r < S.n; r += gstride())
+        if (!(S.diag[r] > 0.0)) atomicMin(first_bad, (unsigned long long)r);
+}
+
+__global__ void k_check_diag_final(SysView S, DevScalars *sc, const unsigned long long *first_bad) {
+    if (*first_bad != ~0ULL) {
+        sc->status = FLIP_E_SINGULAR;
+        sc->err_cell = S.cell ? S.cell[*first_bad] : (long long)*first_bad;
+        sc->done = 1;
+    }
+}
+
+// x += alpha s; r -= alpha q; res = max|r|  (pressure.py:321-323)
+__global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
+                             const double *__restrict__ s, const double *__restrict__ q,
+                             DevScalars *sc) {
+    if (sc->done) return;
+    double alpha = sc->alpha;
+    double m = 0.0;
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        x[i] = x[i] + alpha * s[i];
+        double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        m = fmax(m, fabs(ri));
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(&sc->res_bits, m);
+}
+
+// convergence test after an iteration (pressure.py:324-326 / 211-213)
+__global__ void k_iter_check(DevScalars *sc, int64_t max_iters, double *history) {
+    if (sc->done) return;
+    int it = sc->iter + 1;
+    sc->iter = it;
+    double res = __longlong_as_double((long long)sc->res_bits);
+    sc->res = res;
+    sc->res_bits = 0;
+    if (history) history[it - 1] = res;
+    if (res <= sc->target) {
+        sc->done = 1;
+        sc->converged = 1;
+    } else if (it >= max_iters) {
+        sc->done = 1;
+        sc->converged = 0;
+    }
+}
+
+// z = r * inv_diag (Jacobi preconditioner, pressure.py:289-293) or z = r
+__global__ void k_precond_diag(int64_t n, const double *__restrict__ r, const double *__restrict__ pc,
+                               double *__restrict__ z, const DevScalars *sc, int check_done) {
+    if (check_done && sc->done) return;
+    for (int64_t i = gtid(); i < n; i += gstride()) z[i] = pc ? r[i] * pc[i] : r[i];
+}
+
+__global__ void k_inv_diag(int64_t n, const double *__restrict__ diag, double scale,
+                           double *__restrict__ pc) {
+    for (int64_t i = gtid(); i < n; i += gstride()) pc[i] = 1.0 / (scale * diag[i]);
+}
+
+// s = z + beta s (pressure.py:329)
+__global__ void k_pcg_dir(int64_t n, double *__restrict__ s, const double *__restrict__ z,
+                          const DevScalars *sc) {
+    if (sc->done) return;
+    double beta = sc->beta;
+    for (int64_t i = gtid(); i < n; i += gstride()) s[i] = z[i] + beta * s[i];
+}
+
+__global__ void k_fill(double *a, int64_t n, double v) {
+    for (int64_t i = gtid(); i < n; i += gstride()) a[i] = v;
+}
+
+// ---- solver driver ----
+struct SolveBufs {
+    double *x, *r, *z, *s, *q, *tq, *precon, *xtmp, *dot_tmp;
+    int *scan_tmp;
+    unsigned long long *u64_scratch;  // >= 1
+};
+
+struct SolveCfg {
+    int solver, precond;
+    int64_t max_iters;
+    double tol;
+    int check_every;
+    double *history;  // device, may be null
+    // RBGS colours: explicit row lists (plugin API) or parity of the row's
+    // cell (assembled systems, pressure.py:166-170)
+    const int *red, *black;
+    int64_t nred, nblack;
+    Dims d;
+};
+
+struct SolveOut {
+    int64_t iterations;
+    double residual;
+    int converged;
+    int status;
+    int64_t err_cell, err_it;
+    double err_value;
+};
+
+template <int MODE>
+static void sweep(const SysView &S, const Levels &L, int reverse, const double *src, double *dst,
+                  const double *precon, DevScalars *sc, int check_done, cudaStream_t st,
+                  int64_t *launches) {
+    SweepArgs A{S, L.rows, L.off, L.nlev, reverse, 0.97, 0.25, src, dst, precon, sc, check_done};
+    launch_sweep<MODE>(A, st);
+    (*launches)++;
+}
+
+// Levels for the three sweep kinds: fwd (MIC build / forward), bwd (MIC
+// backward, with reverse flag) and gs.  For assembled systems all three are
+// the geometric hyperplanes (bwd = fwd reversed).
+struct SweepLevels {
+    const Levels *fwd, *bwd, *gs;
+    int bwd_reverse;
+};
+
+// z = M^-1 r for the selected preconditioner (pressure.py:284-300).
+static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
+                     const SweepLevels &LV, const double *r, double *z, DevScalars *sc,
+                     cudaStream_t st, int64_t *launches) {
+    if (cfg.precond == FLIP_PRECOND_MIC0) {
+        // forward substitution into tq (zero-initialised reads are handled
+        // by the k < r guard), then backward into z
+        sweep<SW_MIC_FWD>(S, *LV.fwd, 0, r, B.tq, B.precon, sc, 1, st, launches);
+        sweep<SW_MIC_BWD>(S, *LV.bwd, LV.bwd_reverse, B.tq, z, B.precon, sc, 1, st, launches);
+    } else {
+        k_precond_diag<<<nblocks(S.n), kThreads, 0, st>>>(
+            S.n, r, cfg.precond == FLIP_PRECOND_JACOBI ? B.precon : nullptr, z, sc, 1);
+        (*launches)++;
+    }
+}
+
+// Runs SOLVERS[solver](sys, max_iters, tol) (pressure.py:200-332) on the
+// device.  sc->rhsmax_bits must hold max|rhs|.  Host syncs once per
+// check_every iterations to poll the done flag.
+static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
+                     const SweepLevels &LV, DevScalars *sc, DevScalars *sch, cudaStream_t st,
+                     int64_t *launches, SolveOut *out) {
+    int64_t n = S.n;
+    bool relax = cfg.solver != FLIP_SOLVER_PCG;
+    k_solve_init<<<1, 1, 0, st>>>(sc, cfg.tol, n, relax ? 1 : 0);
+    cudaMemsetAsync(B.u64_scratch, 0xff, sizeof(unsigned long long), st);
+    (*launches)++;
+    if (n > 0) {
+        k_check_diag<<<nblocks(n), kThreads, 0, st>>>(S, sc, B.u64_scratch);
+        k_check_diag_final<<<1, 1, 0, st>>>(S, sc, B.u64_scratch);
+        *launches += 2;
+        k_fill<<<nblocks(n), kThreads, 0, st>>>(B.x, n, 0.0);
+        (*launches)++;
+    }
+    int every = cfg.check_every > 0 ? cfg.check_every : (relax ? 64 : 8);
+    if (n > 0 && !relax) {
+        if (cfg.precond == FLIP_PRECOND_MIC0)
+            sweep<SW_MIC_BUILD>(S, *LV.fwd, 0, nullptr, B.precon, nullptr, sc, 1, st, launches);
+        else if (cfg.precond == FLIP_PRECOND_JACOBI) {
+            k_inv_diag<<<nblocks(n), kThreads, 0, st>>>(n, S.diag, S.scale, B.precon);
+            (*launches)++;
+        }
+        cudaMemcpyAsync(B.r, S.rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+        apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches);
+        cudaMemcpyAsync(B.s, B.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+        launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA0, sc, st, launches);
+    }
+    int64_t it = 0;
+    while (n > 0 && it < cfg.max_iters) {
+        int64_t batch = std::min<int64_t>(every, cfg.max_iters - it);
+        for (int64_t b = 0; b < batch; b++) {
+            if (!relax) {  // pressure.py:314-331
+                k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr, nullptr, sc, 1);
+                launch_dot(B.s, B.q, n, B.dot_tmp, nullptr, EPI_CURV, sc, st, launches);
+                k_pcg_update<<<nblocks(n), kThreads, 0, st>>>(n, B.x, B.r, B.s, B.q, sc);
+                k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
+                apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches);
+                launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA_NEW, sc, st, launches);
+                k_pcg_dir<<<nblocks(n), kThreads, 0, st>>>(n, B.s, B.z, sc);
+                *launches += 4;
+            } else {  // pressure.py:209-213
+                if (cfg.solver == FLIP_SOLVER_JACOBI) {
+                    k_jacobi<<<nblocks(n), kThreads, 0, st>>>(S, B.x, B.xtmp, sc, 1);
+                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.xtmp, nullptr, S.rhs, &sc->res_bits,
+                                                              B.x, sc, 1);
+                    *launches += 2;
+                } else {
+                    if (cfg.solver == FLIP_SOLVER_GS) {
+                        sweep<SW_GS>(S, *LV.gs, 0, nullptr, B.x, nullptr, sc, 1, st, launches);
+                    } else {
+                        k_gs_rows<<<nblocks(cfg.red ? cfg.nred : n), kThreads, 0, st>>>(
+                            S, cfg.red, cfg.nred, 0, cfg.d, B.x, sc, 1);
+                        k_gs_rows<<<nblocks(cfg.black ? cfg.nblack : n), kThreads, 0, st>>>(
+                            S, cfg.black, cfg.nblack, 1, cfg.d, B.x, sc, 1);
+                        *launches += 2;
+                    }
+                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.x, nullptr, S.rhs, &sc->res_bits,
+                                                              nullptr, sc, 1);
+                    (*launches)++;
+                }
+                k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
+                (*launches)++;
+            }
+        }
+        it += batch;
+        cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
+        FLIP_CUDA_OK(cudaStreamSynchronize(st));
+        if (sch->done) break;
+    }
+    cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
+    FLIP_CUDA_OK(cudaStreamSynchronize(st));
+    FLIP_CUDA_OK(cudaGetLastError());
+    out->iterations = sch->iter;
+    out->residual = sch->res;
+    out->converged = sch->converged;
+    out->status = sch->status;
+    out->err_cell = sch->err_cell;
+    out->err_it = sch->err_it;
+    out->err_value = sch->err_value;
+    return 0;
+}
+
+
+// ============================================================ step: project
+// assemble (pressure.py:76-166) + SOLVERS[cfg.solver] (sim.py:266-270) +
+// grid.p = pressure_field(x) (sim.py:274).  Syncs to learn the row count.
+int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
+    cudaStream_t st = c.st;
+    int64_t nc = c.ncells;
+    cudaMemsetAsync(&c.sc->npinned, 0, sizeof(int), st);
+    cudaMemsetAsync(&c.sc->rhsmax_bits, 0, sizeof(unsigned long long), st);
+    k_uf_init<<<nblocks(nc), kThreads, 0, st>>>(c.label, nc, c.parent, c.has_air);
+    k_uf_link<<<nblocks(nc), kThreads, 0, st>>>(c.label, c.d, c.parent);
+    k_uf_finish<<<nblocks(nc), kThreads, 0, st>>>(c.label, c.d, c.parent, c.has_air);
+    IsRowIn in{c.label, c.parent, c.has_air};
+    exclusive_scan(in, nc, c.rowscan, &c.sc->nrows, c.scan_tmp, st);
+    k_rows_compact<<<nblocks(nc), kThreads, 0, st>>>(in, nc, c.rowscan, c.isrow, c.cell_of_row, c.sc);
+    k_assemble_rows<<<nblocks(nc), kThreads, 0, st>>>(c.d, c.label, c.isrow, c.rowscan,
+                                                      c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr, nc,
+                                                      c.diagd, c.rhs, &c.sc->rhsmax_bits);
+    c.launches += 8;
+    cudaMemcpyAsync(c.sch, c.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
+    FLIP_CUDA_OK(cudaStreamSynchronize(st));
+    int64_t n = c.sch->nrows;
+    double dt = c.sch->dt;
+    rep->nrows = n;
+    rep->npinned = c.sch->npinned;
+    // scale = dt / (rho * dtau**2) (pressure.py:164), same IEEE division as the reference
+    double scale = dt / prm.rho_dtau2_h;
+    SysView S{n, c.cell_of_row, c.nbr, nc, c.diagd, c.rhs, scale};
+    bool need_levels = prm.solver == FLIP_SOLVER_GS ||
+                       (prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MIC0);
+    Levels L{c.lvl, c.lvl_cnt, c.lvl_off, c.lvl_rows, &c.sc->nlevels, 0};
+    if (need_levels && n > 0) {
+        int maxl = c.d.nx + c.d.ny + c.d.nz - 2;
+        cudaMemsetAsync(c.lvl_cnt, 0, sizeof(int) * (maxl + 1), st);
+        k_lvl_geom<<<nblocks(n), kThreads, 0, st>>>(c.cell_of_row, n, c.d, c.lvl, c.lvl_cnt);
+        bucket_levels(L, n, maxl, c.scan_tmp, st, &c.launches);
+        k_set_nlevels<<<1, 1, 0, st>>>(c.sc, maxl);
+        c.launches += 2;
+    }
+    SweepLevels LV{&L, &L, &L, 1};
+    SolveCfg cfg{prm.solver, prm.precond, prm.max_iters, prm.tol, prm.solver_check_every, nullptr,
+                 nullptr, nullptr, 0, 0, c.d};
+    SolveBufs B{c.x, c.r, c.z, c.s, c.q, c.tq, c.precon, c.xtmp, c.dot_part, c.scan_tmp,
+                c.u64_scratch};
+    SolveOut o{};
+    int rc = run_solve(S, cfg, B, LV, c.sc, c.sch, st, &c.launches, &o);
+    if (rc) return rc;
+    rep->solver_iterations = o.iterations;
+    rep->solver_residual = o.residual;
+    rep->solver_converged = o.converged;
+    rep->status = o.status;
+    rep->err_cell = o.err_cell;
+    rep->err_iteration = o.err_it;
+    rep->err_value = o.err_value;
+    if (o.status) return 0;
+    k_pressure_field<<<nblocks(nc), kThreads, 0, st>>>(c.p, nc, c.isrow, c.rowscan, c.x);
+    c.launches++;
+    return 0;
+}
+
+// ======================================================= plugin API solves
+__global__ void k_i64_to_i32(const long long *__restrict__ a, int *__restrict__ b, int64_t n) {
+    for (int64_t i = gtid(); i < n; i += gstride()) b[i] = (int)a[i];
+}
+
+// (n,6) row-major int64 -> [6][n] int32
+__global__ void k_nbr_transpose(const long long *__restrict__ a, int *__restrict__ b, int64_t n) {
+    for (int64_t i = gtid(); i < n * 6; i += gstride()) {
+        int64_t r = i / 6, q = i % 6;
+        b[q * n + r] = (int)a[i];
+    }
+}
+
+__global__ void k_absmax(const double *__restrict__ a, int64_t n, unsigned long long *out) {
+    double m = 0.0;
+    for (int64_t i = gtid(); i < n; i += gstride()) m = fmax(m, fabs(a[i]));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(out, m);
+}
+
+// Device scratch for one plugin-API call, freed on scope exit.
+struct DevArena {
+    std::vector<void *> ptrs;
+    ~DevArena() {
+        for (void *p : ptrs) cudaFree(p);
+    }
+    template <class T>
+    T *get(int64_t n) {
+        void *p = nullptr;
+        if (cudaMalloc(&p, sizeof(T) * (size_t)(n > 0 ? n : 1)) != cudaSuccess) return nullptr;
+        ptrs.push_back(p);
+        return (T *)p;
+    }
+};
+
+// Generic levels by relaxation; returns 0 or a CUDA error code.
+static int generic_levels(DevArena &ar, const SysView &S, int mode, Levels &L, cudaStream_t st,
+                          int *scan_tmp) {
+    int64_t n = S.n;
+    L.lvl = ar.get<int>(n);
+    L.rows = ar.get<int>(n);
+    L.cnt = ar.get<int>(n + 1);
+    L.off = ar.get<int>(n + 2);
+    L.nlev = ar.get<int>(2);
+    L.reverse = 0;
+    int *changed = ar.get<int>(1);
+    if (!L.lvl || !L.rows || !L.cnt || !L.off || !L.nlev || !changed) {
+        set_error("cudaMalloc failed (levels)");
+        return FLIP_E_CUDA;
+    }
+    cudaMemsetAsync(L.lvl, 0, sizeof(int) * n, st);
+    int h = 1;
+    int64_t guard = 0;
+    while (h) {
+        cudaMemsetAsync(changed, 0, sizeof(int), st);
+        k_lvl_relax<<<nblocks(n), kThreads, 0, st>>>(S, mode, L.lvl, changed);
+        FLIP_CUDA_OK(cudaMemcpyAsync(&h, changed, sizeof(int), cudaMemcpyDeviceToHost, st));
+        FLIP_CUDA_OK(cudaStreamSynchronize(st));
+        if (++guard > 4 * n + 8) {
+            set_error("level schedule did not converge");
+            return FLIP_E_ARG;
+        }
+    }
+    cudaMemsetAsync(L.cnt, 0, sizeof(int) * (n + 1), st);
+    cudaMemsetAsync(L.nlev + 1, 0xff, sizeof(int), st);
+    k_lvl_count<<<nblocks(n), kThreads, 0, st>>>(L.lvl, n, L.cnt, L.nlev + 1);
+    int64_t dummy = 0;
+    bucket_levels(L, n, (int)n, scan_tmp, st, &dummy);
+    k_nlev_from_max<<<1, 1, 0, st>>>(L.nlev);
+    return 0;
+}
+
+
+}  // namespace flip
+
+using namespace flip;
+
+// ---------------------------------------------------- extern "C" plugin API
+namespace {
+
+struct ApiStream {
+    cudaStream_t st = nullptr;
+    ApiStream() { cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking); }
+    ~ApiStream() {
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
+#define API_CHECK(expr) FLIP_CUDA_OK(expr)
+
+// Uploads an (n,6) int64 neighbour table as [6][n] int32.
+int upload_nbr(DevArena &ar, const int64_t *nbr_rows, int64_t n, int **out, cudaStream_t st) {
+    long long *tmp = ar.get<long long>(n * 6);
+    int *d = ar.get<int>(n * 6);
+    if (!tmp || !d) {
+        set_error("cudaMalloc failed");
+        return FLIP_E_CUDA;
+    }
+    API_CHECK(cudaMemcpyAsync(tmp, nbr_rows, sizeof(int64_t) * n * 6, cudaMemcpyHostToDevice, st));
+    if (n > 0) k_nbr_transpose<<<nblocks(n * 6), kThreads, 0, st>>>(tmp, d, n);
+    *out = d;
+    return 0;
+}
+
+double *upload_d(DevArena &ar, const double *h, int64_t n, cudaStream_t st) {
+    double *d = ar.get<double>(n);
+    if (d && n > 0) cudaMemcpyAsync(d, h, sizeof(double) * n, cudaMemcpyHostToDevice, st);
+    return d;
+}
+
+}  // namespace
+
+extern "C" int flip_k_laplacian_matvec(int64_t n, const double *diag, const int64_t *nbr_rows,
+                                       const double *x, double scale, double *y) {
+    ApiStream S;
+    DevArena ar;
+    int *nb = nullptr;
+    if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
+    double *dd = upload_d(ar, diag, n, S.st), *dx = upload_d(ar, x, n, S.st), *dy = ar.get<double>(n);
+    SysView V{n, nullptr, nb, n, dd, nullptr, scale};
+    if (n > 0) k_matvec<<<nblocks(n), kThreads, 0, S.st>>>(V, dx, dy, nullptr, nullptr, nullptr, nullptr, 0);
+    API_CHECK(cudaMemcpyAsync(y, dy, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+    API_CHECK(cudaStreamSynchronize(S.st));
+    API_CHECK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int flip_k_jacobi_iter(int64_t n, const double *diag, const int64_t *nbr_rows,
+                                  const double *rhs, const double *x, double scale, double *out) {
+    ApiStream S;
+    DevArena ar;
+    int *nb = nullptr;
+    if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
+    double *dd = upload_d(ar, diag, n, S.st), *dr = upload_d(ar, rhs, n, S.st),
+           *dx = upload_d(ar, x, n, S.st), *dout = ar.get<double>(n);
+    SysView V{n, nullptr, nb, n, dd, dr, scale};
+    if (n > 0) k_jacobi<<<nblocks(n), kThreads, 0, S.st>>>(V, dx, dout, nullptr, 0);
+    API_CHECK(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+    API_CHECK(cudaStreamSynchronize(S.st));
+    API_CHECK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int flip_k_gs_sweep_rows(int64_t m, const int64_t *rows, int64_t n, const double *diag,
+                                    const int64_t *nbr_rows, const double *rhs, double *x,
+                                    double scale) {
+    ApiStream S;
+    DevArena ar;
+    int *nb = nullptr;
+    if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
+    double *dd = upload_d(ar, diag, n, S.st), *dr = upload_d(ar, rhs, n, S.st),
+           *dx = upload_d(ar, x, n, S.st);
+    long long *r64 = ar.get<long long>(m);
+    int *r32 = ar.get<int>(m);
+    API_CHECK(cudaMemcpyAsync(r64, rows, sizeof(int64_t) * m, cudaMemcpyHostToDevice, S.st));
+    if (m > 0) {
+        k_i64_to_i32<<<nblocks(m), kThreads, 0, S.st>>>(r64, r32, m);
+        SysView V{n, nullptr, nb, n, dd, dr, scale};
+        k_gs_rows<<<nblocks(m), kThreads, 0, S.st>>>(V, r32, m, 0, Dims{}, dx, nullptr, 0);
+    }
+    API_CHECK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+    API_CHECK(cudaStreamSynchronize(S.st));
+    API_CHECK(cudaGetLastError());
+    return 0;
+}
+
+// Wavefront kernels of the plugin API use generic (relaxed) level schedules.
+static int api_sweep(int mode, int64_t n, const double *diag, const int64_t *nbr_rows,
+                     const double *rhs, const double *src_h, const double *precon_h, double scale,
+                     double *out_h, const double *xin_h) {
+    ApiStream S;
+    DevArena ar;
+    int *nb = nullptr;
+    if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
+    double *dd = diag ? upload_d(ar, diag, n, S.st) : nullptr;
+    double *dr = rhs ? upload_d(ar, rhs, n, S.st) : nullptr;
+    double *dsrc = src_h ? upload_d(ar, src_h, n, S.st) : nullptr;
+    double *dpc = precon_h ? upload_d(ar, precon_h, n, S.st) : nullptr;
+    double *tq = ar.get<double>(n), *dout = xin_h ? upload_d(ar, xin_h, n, S.st) : ar.get<double>(n);
+    int *scan_tmp = ar.get<int>(scan_tmp_ints(n + 2) + 8);
+    if (n == 0) return 0;
+    SysView V{n, nullptr, nb, n, dd, dr, scale};
+    if (mode == SW_MIC_FWD) {  // full apply: forward into tq, backward into out
+        Levels Lf{}, Lb{};
+        if (int rc = generic_levels(ar, V, 0, Lf, S.st, scan_tmp)) return rc;
+        if (int rc = generic_levels(ar, V, 1, Lb, S.st, scan_tmp)) return rc;
+        SweepArgs A{V, Lf.rows, Lf.off, Lf.nlev, 0, 0.97, 0.25, dsrc, tq, dpc, nullptr, 0};
+        API_CHECK(launch_sweep<SW_MIC_FWD>(A, S.st));
+        SweepArgs B{V, Lb.rows, Lb.off, Lb.nlev, 0, 0.97, 0.25, tq, dout, dpc, nullptr, 0};
+        API_CHECK(launch_sweep<SW_MIC_BWD>(B, S.st));
+    } else {
+        Levels L{};  // SW_GS
+        if (int rc = generic_levels(ar, V, 2, L, S.st, scan_tmp)) return rc;
+        SweepArgs A{V, L.rows, L.off, L.nlev, 0, 0.97, 0.25, dsrc, dout, dpc, nullptr, 0};
+        API_CHECK(launch_sweep<SW_GS>(A, S.st));
+    }
+    API_CHECK(cudaMemcpyAsync(out_h, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+    API_CHECK(cudaStreamSynchronize(S.st));
+    API_CHECK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int flip_k_gs_sweep(int64_t n, const double *diag, const int64_t *nbr_rows,
+                               const double *rhs, double *x, double scale) {
+    return api_sweep(SW_GS, n, diag, nbr_rows, rhs, nullptr, nullptr, scale, x, x);
+}
+
+extern "C" int flip_k_mic0_apply(int64_t n, const double *precon, const int64_t *nbr_rows,
+                                 const double *r, double scale, double *z) {
+    return api_sweep(SW_MIC_FWD, n, nullptr, nbr_rows, nullptr, r, precon, scale, z, nullptr);
+}
+
+extern "C" int flip_k_mic0_build(int64_t n, const double *diag, const int64_t *nbr_rows,
+                                 double scale, double tau, double sigma, double *precon) {
+    ApiStream S;
+    DevArena ar;
+    int *nb = nullptr;
+    if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
+    double *dd = upload_d(ar, diag, n, S.st), *dout = ar.get<double>(n);
+    int *scan_tmp = ar.get<int>(scan_tmp_ints(n + 2) + 8);
+    if (n == 0) return 0;
+    SysView V{n, nullptr, nb, n, dd, nullptr, scale};
+    Levels L{};
+    if (int rc = generic_levels(ar, V, 0, L, S.st, scan_tmp)) return rc;
+    SweepArgs A{V, L.rows, L.off, L.nlev, 0, tau, sigma, nullptr, dout, nullptr, nullptr, 0};
+    API_CHECK(launch_sweep<SW_MIC_BUILD>(A, S.st));
+    API_CHECK(cudaMemcpyAsync(precon, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+    API_CHECK(cudaStreamSynchronize(S.st));
+    API_CHECK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int flip_k_pairwise_dot(int64_t n, const double *a, const double *b, double *out) {
+    ApiStream S;
+    DevArena ar;
+    double *da = upload_d(ar, a, n, S.st), *db = b ? upload_d(ar, b, n, S.st) : nullptr;
+    double *tmp = ar.get<double>(dot_tmp_doubles(n)), *res = ar.get<double>(1);
+    int64_t l = 0;
+    if (n == 0) {
+        *out = 0.0;
+        return 0;
+    }
+    launch_pairwise_dot(da, db, n, tmp, res, S.st, &l);
+    API_CHECK(cudaMemcpyAsync(out, res, sizeof(double), cudaMemcpyDeviceToHost, S.st));
+    API_CHECK(cudaStreamSynchronize(S.st));
+    API_CHECK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, const int64_t *cells,
+                                 const double *diag, const int64_t *nbr_rows, const double *rhs,
+                                 double scale, int64_t max_iters, double tol,
+                                 const int64_t *red_rows, int64_t nred, const int64_t *black_rows,
+                                 int64_t nblack, double *x, int64_t *iterations, double *residual,
+                                 int32_t *converged, int64_t *err_cell, int64_t *err_iteration,
+                                 double *err_value) {
+    if (solver < 0 || solver > 3 || precond < 0 || precond > 2) {
+        set_error("unknown solver or preconditioner");
+        return FLIP_E_CONFIG;
+    }
+    ApiStream S;
+    DevArena ar;
+    int *nb = nullptr;
+    if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
+    double *dd = upload_d(ar, diag, n, S.st), *dr = upload_d(ar, rhs, n, S.st);
+    long long *c64 = ar.get<long long>(n);
+    int *c32 = ar.get<int>(n);
+    API_CHECK(cudaMemcpyAsync(c64, cells, sizeof(int64_t) * n, cudaMemcpyHostToDevice, S.st));
+    if (n > 0) k_i64_to_i32<<<nblocks(n), kThreads, 0, S.st>>>(c64, c32, n);
+    int *red = nullptr, *black = nullptr;
+    if (solver == FLIP_SOLVER_RBGS) {
+        long long *t = ar.get<long long>(nred + nblack);
+        red = ar.get<int>(nred);
+        black = ar.get<int>(nblack);
+        API_CHECK(cudaMemcpyAsync(t, red_rows, sizeof(int64_t) * nred, cudaMemcpyHostToDevice, S.st));
+        API_CHECK(cudaMemcpyAsync(t + nred, black_rows, sizeof(int64_t) * nblack,
+                                  cudaMemcpyHostToDevice, S.st));
+        if (nred) k_i64_to_i32<<<nblocks(nred), kThreads, 0, S.st>>>(t, red, nred);
+        if (nblack) k_i64_to_i32<<<nblocks(nblack), kThreads, 0, S.st>>>(t + nred, black, nblack);
+    }
+    DevScalars *sc = ar.get<DevScalars>(1);
+    DevScalars *sch = nullptr;
+    API_CHECK(cudaMallocHost(&sch, sizeof(DevScalars)));
+    struct HostFree {
+        void *p;
+        ~HostFree() { cudaFreeHost(p); }
+    } hf{sch};
+    API_CHECK(cudaMemsetAsync(sc, 0, sizeof(DevScalars), S.st));
+    if (n > 0) k_absmax<<<nblocks(n), kThreads, 0, S.st>>>(dr, n, &sc->rhsmax_bits);
+    SysView V{n, c32, nb, n, dd, dr, scale};
+    int *scan_tmp = ar.get<int>(scan_tmp_ints(n + 2) + 8);
+    Levels Lf{}, Lb{}, Lg{};
+    bool mic = solver == FLIP_SOLVER_PCG && precond == FLIP_PRECOND_MIC0;
+    if (n > 0 && mic) {
+        if (int rc = generic_levels(ar, V, 0, Lf, S.st, scan_tmp)) return rc;
+        if (int rc = generic_levels(ar, V, 1, Lb, S.st, scan_tmp)) return rc;
+    }
+    if (n > 0 && solver == FLIP_SOLVER_GS)
+        if (int rc = generic_levels(ar, V, 2, Lg, S.st, scan_tmp)) return rc;
+    SweepLevels LV{&Lf, &Lb, &Lg, 0};
+    SolveCfg cfg{solver, precond, max_iters, tol, 0, nullptr, red, black, nred, nblack, Dims{}};
+    SolveBufs B{ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),
+                ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),
+                ar.get<double>(dot_tmp_doubles(n)), scan_tmp, ar.get<unsigned long long>(1)};
+    SolveOut o{};
+    int64_t api_launches = 0;
+    if (int rc = run_solve(V, cfg, B, LV, sc, sch, S.st, &api_launches, &o)) return rc;
+    if (n > 0) API_CHECK(cudaMemcpyAsync(x, B.x, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+    API_CHECK(cudaStreamSynchronize(S.st));
+    API_CHECK(cudaGetLastError());
+    *iterations = o.iterations;
+    *residual = o.residual;
+    *converged = o.converged;
+    *err_cell = o.err_cell;
+    *err_iteration = o.err_it;
+    *err_value = o.err_value;
+    return o.status;
+}

@@ -1,0 +1,297 @@
+"""Drop-in simulation API for the reference's FLIP step (flipsim/sim.py).
+
+``make_scene`` and ``step`` keep the reference's names, arguments, return
+types and error behaviour; all ten stages run as sm_100a kernels in
+libflipb200.so on the state held in one device context.  Host code here only
+validates the spec, evaluates the few Python-float constants the reference
+computes on the host (alpha*dtau, rho*dtau**2, ...), and sizes scene boxes.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _lib, rng
+from ._lib import LIB, check
+from .binning import SpaceHash
+from .device import Device
+from .errors import ConfigError, SingularSystemError, SolverBreakdownError, SolverError
+from .grid import AIR, FLUID, SOLID, GridDims, MacGrid, interior_box_from_labels
+from .particles import ParticleSet, SeedRegion, covered_cells
+
+SCENE_NAMES = ("dam-break", "double-dam-break", "water-drop")
+SOLVERS = ("jacobi", "gs", "rbgs", "pcg")
+PRECONDITIONERS = ("mic0", "jacobi", "none")
+
+
+@dataclass
+class StageTimings:
+    """Device milliseconds per stage (CUDA events on the step stream).
+
+    Keys are the reference's (sim.py:24-46).  P2G and force run as one fused
+    kernel when both are in the step, so ``force`` reads ~0.
+    """
+
+    dt_compute: float = 0.0
+    advect: float = 0.0
+    bin: float = 0.0
+    classify: float = 0.0
+    p2g: float = 0.0
+    force: float = 0.0
+    project: float = 0.0
+    apply_gradient: float = 0.0
+    g2p: float = 0.0
+    reseed: float = 0.0
+
+    @classmethod
+    def stage_names(cls) -> tuple:
+        return tuple(f.name for f in fields(cls))
+
+    def as_dict(self) -> dict:
+        return {f.name: getattr(self, f.name) for f in fields(self)}
+
+    def total(self) -> float:
+        return sum(self.as_dict().values())
+
+
+@dataclass
+class SceneSpec:
+    """Benchmark configuration (sim.py:50-72); ``precond`` is an extension
+    (the reference hard-wires MIC(0), pressure.py:274)."""
+
+    name: str = "dam-break"
+    res: int = 32
+    density: int = 2
+    particle_target: int | None = None
+    gravity: tuple = (0.0, -9.81, 0.0)
+    solver: str = "pcg"
+    tol: float = 1e-6
+    max_iters: int | None = None
+    flip_fraction: float = 0.95
+    alpha: float = 3.0
+    dt_max: float = 1.0 / 30.0
+    rho_fluid: float = 1000.0
+    skin_fraction: float = 1e-3
+    extrapolation_layers: int = 2
+    steps: int = 50
+    precond: str = "mic0"
+
+    def resolved_max_iters(self) -> int:
+        if self.max_iters is not None:
+            return self.max_iters
+        return 100 if self.solver == "pcg" else 2000
+
+
+@dataclass
+class SimState:
+    grid: MacGrid
+    grid_old: MacGrid
+    particles: ParticleSet
+    hash: SpaceHash
+    time: float = 0.0
+    step_count: int = 0
+    rng_seed: int = 0
+    device: Device = field(default=None, repr=False)
+
+
+@dataclass
+class StepReport:
+    timings: StageTimings
+    dt: float
+    particle_count: int
+    solver_iterations: int
+    solver_residual: float
+    solver_converged: bool
+    nrows: int = 0
+    npinned: int = 0
+    gpu_launches: int = 0
+
+
+# ------------------------------------------------------------- scenes ----
+def _fit_box(target, ni, nj, nk, frac_x, frac_y):
+    """(density, cells_x, cells_y) landing near `target` (sim.py:112-132)."""
+    ratio = (frac_x * ni) / (frac_y * nj)
+    best = None
+    for rho in range(1, 11):
+        need = target / rho ** 3 / nk
+        cx0 = np.sqrt(need * ratio)
+        for cx in range(max(1, int(cx0) - 2), min(ni, int(cx0) + 3)):
+            cy_mid = need / cx
+            for cy in range(max(1, int(cy_mid) - 1), min(nj, int(cy_mid) + 3)):
+                err = abs(cx * cy * nk * rho ** 3 - target) / target
+                distort = abs(cx / (frac_x * ni) - 1.0) + abs(cy / (frac_y * nj) - 1.0)
+                key = (err > 0.05, round(err, 6), round(distort, 6), rho)
+                if best is None or key < best[0]:
+                    best = (key, rho, cx, cy)
+    return best[1:]
+
+
+def _box(dims, i0, i1, j0, j1, k0, k1, density):
+    o = np.asarray(dims.origin, dtype=np.float64)
+    return SeedRegion.box(o + np.array([i0, j0, k0]) * dims.dtau,
+                          o + np.array([i1 + 1, j1 + 1, k1 + 1]) * dims.dtau, density)
+
+
+def scene_regions(spec: SceneSpec, dims: GridDims) -> list:
+    """Seed regions of the named scene (sim.py:140-201)."""
+    lo_c, hi_c = 1, spec.res - 2          # one-cell solid shell
+    ni = nj = nk = hi_c - lo_c + 1
+    if ni < 1:
+        raise ConfigError(f"resolution {spec.res} leaves no interior cells")
+    edge = dims.nx * dims.dtau
+    o = np.asarray(dims.origin, dtype=np.float64)
+    tgt = spec.particle_target
+    if spec.name in ("dam-break", "double-dam-break"):
+        double = spec.name == "double-dam-break"
+        if tgt:
+            rho, cx, cy = _fit_box(tgt // 2 if double else tgt, ni, nj, nk, 0.25, 0.75)
+        else:
+            rho, cx, cy = spec.density, max(1, round(0.25 * ni)), max(1, round(0.75 * nj))
+        if not double:
+            return [_box(dims, lo_c, lo_c + cx - 1, lo_c, lo_c + cy - 1, lo_c, hi_c, rho)]
+        cx = min(cx, ni // 2)
+        return [_box(dims, lo_c, lo_c + cx - 1, lo_c, lo_c + cy - 1, lo_c, hi_c, rho),
+                _box(dims, hi_c - cx + 1, hi_c, lo_c, lo_c + cy - 1, lo_c, hi_c, rho)]
+    if spec.name == "water-drop":
+        center = tuple(o + (0.5 * edge, 0.6 * edge, 0.5 * edge))
+        radius = 0.125 * edge
+        pool_cap = max(1, int(0.40 * nj))
+        if tgt:
+            sphere_n = len(covered_cells(SeedRegion.sphere(center, radius, 1), dims))
+            best = None
+            for rho in range(1, 11):
+                py = min(pool_cap, max(1, round((tgt / rho ** 3 - sphere_n) / (ni * nk))))
+                err = abs((py * ni * nk + sphere_n) * rho ** 3 - tgt) / tgt
+                key = (err > 0.05, round(err, 6), rho)
+                if best is None or key < best[0]:
+                    best = (key, rho, py)
+            rho, py = best[1], best[2]
+        else:
+            rho, py = spec.density, max(1, round(0.25 * nj))
+        return [_box(dims, lo_c, hi_c, lo_c, lo_c + py - 1, lo_c, hi_c, rho),
+                SeedRegion.sphere(center, radius, rho)]
+    raise ConfigError(f"unknown scene {spec.name!r}; valid: {SCENE_NAMES}")
+
+
+def _params(cfg: SceneSpec, dtau: float, reseed_seed: int = 0) -> _lib.StepParams:
+    if cfg.solver not in SOLVERS:
+        raise ConfigError(f"unknown solver {cfg.solver!r}; valid: {SOLVERS}")
+    if cfg.precond not in PRECONDITIONERS:
+        raise ValueError(f"unknown preconditioner {cfg.precond!r}")
+    if not 0.0 <= cfg.flip_fraction <= 1.0:           # BlendParams (transfer.py:16-24)
+        raise ValueError("flip_fraction must lie in [0, 1]")
+    assert cfg.alpha > 0 and cfg.dt_max > 0             # particles.py:217
+    skin = cfg.skin_fraction * dtau                     # sim.py:243
+    assert 0 < skin < dtau / 2                          # particles.py:235
+    p = _lib.StepParams()
+    p.gravity[:] = [float(g) for g in cfg.gravity]
+    p.dt_max = float(cfg.dt_max)
+    p.flip_fraction = float(cfg.flip_fraction)
+    p.tol = float(cfg.tol)
+    p.alpha_dtau_h = cfg.alpha * dtau                   # particles.py:224
+    p.rho_dtau2_h = cfg.rho_fluid * dtau ** 2           # pressure.py:164
+    p.rho_dtau_h = cfg.rho_fluid * dtau                 # pressure.py:354
+    p.skin_h = skin
+    p.max_iters = int(cfg.resolved_max_iters())
+    p.solver = _lib.SOLVER_ID[cfg.solver]
+    p.precond = _lib.PRECOND_ID[cfg.precond]
+    p.extrapolation_layers = int(cfg.extrapolation_layers)
+    p.density = int(cfg.density)
+    p.reseed_seed = int(reseed_seed) & rng.MASK64
+    p.solver_check_every = 0
+    return p
+
+
+def make_scene(spec: SceneSpec, rng_seed: int = 0, device: int = 0,
+               capacity: int = 0) -> SimState:
+    """Initial state of a named scene, built on the device (sim.py:204-223)."""
+    if spec.name not in SCENE_NAMES:
+        raise ConfigError(f"unknown scene {spec.name!r}; valid: {SCENE_NAMES}")
+    if spec.solver not in SOLVERS:
+        raise ConfigError(f"unknown solver {spec.solver!r}; valid: {SOLVERS}")
+    dims = GridDims(spec.res, spec.res, spec.res, 1.0 / spec.res)
+    regions = scene_regions(spec, dims)
+    dev = Device(dims, capacity=capacity, device=device)
+    check(LIB.flip_set_solid_shell(dev.ctx), "flip_set_solid_shell")
+    arr = (_lib.Region * len(regions))(*[r.to_c() for r in regions])
+    check(LIB.flip_seed_regions(dev.ctx, len(regions), arr, int(rng_seed) & rng.MASK64),
+          "flip_seed_regions")
+    spec.density = regions[0].density                   # sim.py:219
+    rc, _ = dev.run_stages(_params(spec, dims.dtau), _lib.STAGE["bin"], _lib.STAGE["classify"])
+    check(rc, "make_scene bin/classify")
+    # grid_old = grid.clone(): velocities are zero on both; p/label snapshot
+    old_p = np.zeros(dims.ncells)
+    old_p.flags.writeable = False
+    old_label = np.array(dev.grid_array("label"))
+    old_label.flags.writeable = False
+    return SimState(grid=MacGrid(dev, "grid"), grid_old=MacGrid(dev, "old", old_p, old_label),
+                    particles=ParticleSet(device=dev), hash=SpaceHash(device=dev),
+                    rng_seed=rng_seed, device=dev)
+
+
+def _raise_solver(state: SimState, rep) -> None:
+    if rep.status == _lib.FLIP_E_SINGULAR:
+        inner = SingularSystemError(int(rep.err_cell))
+    else:
+        inner = SolverBreakdownError(
+            f"conjugate-gradient breakdown: curvature {rep.err_value:.3e} "
+            f"at iteration {int(rep.err_iteration)}")
+    raise SolverError(f"step {state.step_count}: {inner}") from inner    # sim.py:269-270
+
+
+def step(state: SimState, cfg: SceneSpec) -> StepReport:
+    """Advance one timestep on the device (sim.py:226-300)."""
+    dev = state.device
+    seed = rng.derive_seed(state.rng_seed, state.step_count + 1)     # sim.py:291
+    params = _params(cfg, dev.dims.dtau, seed)
+    rc, rep = dev.run_stages(params, 0, _lib.NSTAGES - 1)
+    if rc in (_lib.FLIP_E_SINGULAR, _lib.FLIP_E_BREAKDOWN):
+        _raise_solver(state, rep)
+    check(rc, "flip_step")
+    timings = StageTimings(**{n: float(rep.stage_ms[i]) for i, n in enumerate(_lib.STAGE_NAMES)})
+    state.time += rep.dt
+    state.step_count += 1
+    return StepReport(timings=timings, dt=float(rep.dt), particle_count=int(rep.particle_count),
+                      solver_iterations=int(rep.solver_iterations),
+                      solver_residual=float(rep.solver_residual),
+                      solver_converged=bool(rep.solver_converged), nrows=int(rep.nrows),
+                      npinned=int(rep.npinned), gpu_launches=int(rep.gpu_launches))
+
+
+def run_stages(state: SimState, cfg: SceneSpec, first: str, last: str):
+    """Run the named stage range only (per-stage parity / profiling)."""
+    dev = state.device
+    seed = rng.derive_seed(state.rng_seed, state.step_count + 1)
+    rc, rep = dev.run_stages(_params(cfg, dev.dims.dtau, seed), _lib.STAGE[first], _lib.STAGE[last])
+    if rc in (_lib.FLIP_E_SINGULAR, _lib.FLIP_E_BREAKDOWN):
+        _raise_solver(state, rep)
+    check(rc, "flip_run_stages")
+    return rep
+
+
+def total_energy(particles: ParticleSet, g, floor_y: float = 0.0) -> float:
+    """Kinetic + gravitational potential energy per unit mass (sim.py:303-315),
+    with numpy's pairwise summation order (evaluated on the device for
+    device-resident sets)."""
+    if particles.count == 0:
+        return 0.0
+    g_mag = float(np.linalg.norm(np.asarray(g, dtype=np.float64)))
+    if particles._dev is not None:
+        ke2, pe = particles._dev.energy_sums(floor_y)
+    else:
+        ke2 = float(np.add.reduce(particles.vel_x ** 2 + particles.vel_y ** 2 + particles.vel_z ** 2))
+        pe = float(np.add.reduce(particles.pos_y - floor_y))
+    return 0.5 * ke2 + g_mag * pe
+
+
+def energy_floor(state: SimState) -> float:
+    lo, _hi = interior_box_from_labels(state.grid.label, state.grid.dims)
+    return float(lo[1])
+
+
+def divergence_field(state: SimState) -> np.ndarray:
+    """divergence_field(state.grid) (grid.py:147-156) computed on the device."""
+    return state.device.divergence_field()

@@ -1,0 +1,156 @@
+"""GPU parity: the CUDA step against the CPU oracle, bit for bit.
+
+The oracle (oracle/flip_oracle.c) is itself pinned to the reference
+(tests/test_oracle_pins.py).  Everything here compares raw bytes: labels,
+hash counts/offsets, particle order and every float64 field.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import device_arrays, diff_report, oracle_arrays, spec_pair, upload
+
+pytestmark = pytest.mark.gpu
+
+STEP_CASES = [
+    dict(name="dam-break", res=12, solver="pcg"),
+    dict(name="dam-break", res=16, solver="jacobi"),
+    dict(name="double-dam-break", res=16, solver="rbgs"),
+    dict(name="water-drop", res=16, solver="gs"),
+    dict(name="dam-break", res=24, solver="pcg"),
+    dict(name="water-drop", res=20, solver="pcg", particle_target=20000),
+    dict(name="dam-break", res=20, solver="pcg", precond="jacobi"),
+    dict(name="double-dam-break", res=18, solver="pcg", precond="none", flip_fraction=0.0),
+]
+
+
+def _ids(c):
+    return "-".join(f"{v}" for v in c.values())
+
+
+@pytest.mark.parametrize("case", STEP_CASES, ids=[_ids(c) for c in STEP_CASES])
+def test_make_scene_and_steps_bit_exact(pkg, case):
+    dspec, ospec = spec_pair(**case)
+    st = pkg.make_scene(dspec, rng_seed=3)
+    os_ = O.make_scene(ospec, rng_seed=3)
+    assert dspec.density == ospec.density
+    bad = diff_report(device_arrays(st), oracle_arrays(os_))
+    assert not bad, f"make_scene: {bad}"
+    for k in range(5):
+        rep = pkg.step(st, dspec)
+        ref = O.step(os_, ospec)
+        bad = diff_report(device_arrays(st), oracle_arrays(os_))
+        assert not bad, f"step {k}: {bad}"
+        assert rep.dt == ref["dt"]
+        assert rep.particle_count == ref["particle_count"]
+        assert rep.solver_iterations == ref["solver_iterations"]
+        assert rep.solver_residual == ref["solver_residual"]
+        assert rep.solver_converged == ref["solver_converged"]
+        assert st.time == os_.time and st.step_count == os_.step_count
+
+
+def _stage_snapshots(os_, ospec):
+    snaps = {"start": os_.copy()}
+    extras = {}
+
+    def hook(name, st, extra):
+        snaps[name] = st.copy()
+        extras[name] = extra
+
+    O.step(os_, ospec, hook=hook)
+    return snaps, extras
+
+
+@pytest.mark.parametrize("case", STEP_CASES[:5], ids=[_ids(c) for c in STEP_CASES[:5]])
+def test_each_stage_bit_exact(pkg, case):
+    """Upload the oracle's state before each stage, run that stage alone on
+    the device, compare with the oracle's state after it."""
+    dspec, ospec = spec_pair(**case)
+    st = pkg.make_scene(dspec, rng_seed=5)
+    os_ = O.make_scene(ospec, rng_seed=5)
+    for _ in range(2):  # get off the degenerate all-zero first step
+        O.step(os_, ospec)
+    snaps, extras = _stage_snapshots(os_, ospec)
+    dt = extras["dt_compute"]["dt"]
+    known = extras["p2g"]["known"]
+    order = ["start"] + list(O.STAGES)
+    for prev, name in zip(order[:-1], order[1:]):
+        before = snaps[prev].copy()
+        after = snaps[name]
+        if name == "apply_gradient":
+            sys_, res = extras["project"]["system"], extras["project"]["result"]
+            before.p = O.pressure_field(sys_, res["p"], before.dims.ncells)
+        st.step_count = before.step_count
+        upload(st, before, dt=None if name == "dt_compute" else dt,
+               known=known if name == "apply_gradient" else None)
+        rep = pkg.run_stages(st, dspec, name, name)
+        ref = oracle_arrays(after)
+        if name == "project":  # the device writes p = pressure_field(x) here
+            sys_, res = extras["project"]["system"], extras["project"]["result"]
+            ref["p"] = O.pressure_field(sys_, res["p"], after.dims.ncells)
+            assert rep.solver_iterations == res["iterations"]
+            assert rep.solver_residual == res["residual"]
+            assert rep.nrows == sys_.nrows
+        if name == "advect":
+            # the device fuses cell_index + bincount into advect, so count
+            # already holds the BIN stage's histogram of the moved particles
+            cells = np.empty(after.n, dtype=np.int64)
+            O.lib().orc_cell_index_many(after.dims.c(), after.n, O._p(after.parts[0]),
+                                        O._p(after.parts[1]), O._p(after.parts[2]),
+                                        O._p(cells, O._i64))
+            ref["count"] = np.bincount(cells, minlength=after.dims.ncells)
+        bad = diff_report(device_arrays(st), ref)
+        assert not bad, f"stage {name}: {bad}"
+        if name == "dt_compute":
+            assert st.device.dt() == dt
+        if name == "p2g":
+            got = st.device.known()
+            for g, k in zip(got, known):
+                assert np.array_equal(g, k.astype(bool))
+
+
+def test_gpu_reseed_fast_path_keeps_state(pkg):
+    """A rest state with zero gravity is a bit-exact fixed point (test_sim.py:69-77)."""
+    dspec, _ = spec_pair(name="dam-break", res=12, gravity=(0.0, 0.0, 0.0))
+    st = pkg.make_scene(dspec, rng_seed=2)
+    before = [a.tobytes() for a in st.particles.arrays()]
+    rep = pkg.step(st, dspec)
+    assert [a.tobytes() for a in st.particles.arrays()] == before
+    assert rep.dt == dspec.dt_max
+    assert not st.particles.vel_x.any() and not st.particles.vel_y.any()
+
+
+def test_post_step_divergence_small(pkg):
+    """Projection leaves max|div| <= 1e-4 over FLUID cells (test_sim.py:79-86)."""
+    dspec, _ = spec_pair(name="dam-break", res=16)
+    st = pkg.make_scene(dspec, rng_seed=3)
+    for _ in range(3):
+        pkg.step(st, dspec)
+        div = pkg.divergence_field(st)
+        fluid = st.grid.label == pkg.FLUID
+        assert np.abs(div[fluid]).max() <= 1e-4
+
+
+def test_hash_accounts_for_every_particle(pkg):
+    dspec, _ = spec_pair(name="dam-break", res=12)
+    st = pkg.make_scene(dspec, rng_seed=6)
+    pkg.step(st, dspec)
+    assert st.hash.count.sum() == st.particles.count
+    assert np.array_equal(st.hash.fluid_cells, np.flatnonzero(st.hash.count > 0))
+
+
+def test_energy_matches_oracle_pairwise(pkg):
+    dspec, ospec = spec_pair(name="dam-break", res=16)
+    st = pkg.make_scene(dspec, rng_seed=1)
+    os_ = O.make_scene(ospec, rng_seed=1)
+    for _ in range(3):
+        pkg.step(st, dspec)
+        O.step(os_, ospec)
+    e_dev = pkg.total_energy(st.particles, dspec.gravity, pkg.energy_floor(st))
+    P = os_.parts
+    g = float(np.linalg.norm(np.asarray(dspec.gravity)))
+    floor = 1.0 / 16
+    e_ref = (0.5 * float(np.add.reduce(P[3] ** 2 + P[4] ** 2 + P[5] ** 2))
+             + g * float(np.add.reduce(P[1] - floor)))
+    assert e_dev == e_ref
