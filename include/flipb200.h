@@ -129,6 +129,8 @@ int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, double dtau,
                 const double origin[3], int64_t capacity, flip_ctx **out);
 void flip_destroy(flip_ctx *ctx);
 int flip_synchronize(flip_ctx *ctx);
+/* The cudaStream_t every kernel of this ctx is launched on (for timing). */
+int flip_get_stream(flip_ctx *ctx, void **stream);
 
 /* State transfer (host pointers; NULL entries are skipped). */
 int flip_set_grid(flip_ctx *ctx, const double *u, const double *v, const double *w,
@@ -170,6 +172,9 @@ int flip_run_stages(flip_ctx *ctx, const flip_step_params *params, int32_t first
  * host div[ncells]; total_energy sums (sim.py:303-315) with numpy pairwise
  * order: ke2 = sum(vx^2+vy^2+vz^2), pe = sum(py - floor_y). */
 int flip_divergence_field(flip_ctx *ctx, double *div);
+/* Test hook: copy an internal device buffer ("precon", "x", "rhs", "diag",
+ * "cell_of_row", "rowscan", "nbr", "z", "tq", "r") to host. */
+int flip_debug_copy(flip_ctx *ctx, const char *name, void *host, int64_t bytes);
 int flip_energy_sums(flip_ctx *ctx, double floor_y, double *ke2, double *pe);
 
 /* ---- kernel-backend plugin API (flipsim._kernels module functions) ---- */

@@ -93,6 +93,7 @@ _SIGNATURES = {
                               C.c_int64, C.POINTER(_vp)]),
     "flip_destroy": (None, [_vp]),
     "flip_synchronize": (C.c_int, [_vp]),
+    "flip_get_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "flip_set_grid": (C.c_int, [_vp, _d, _d, _d, _d, _u8]),
     "flip_get_grid": (C.c_int, [_vp, _d, _d, _d, _d, _u8]),
     "flip_set_grid_old": (C.c_int, [_vp, _d, _d, _d]),
@@ -113,6 +114,7 @@ _SIGNATURES = {
     "flip_run_stages": (C.c_int, [_vp, C.POINTER(StepParams), C.c_int32, C.c_int32,
                                   C.POINTER(StepReportC)]),
     "flip_divergence_field": (C.c_int, [_vp, _d]),
+    "flip_debug_copy": (C.c_int, [_vp, C.c_char_p, _vp, C.c_int64]),
     "flip_energy_sums": (C.c_int, [_vp, C.c_double, _d, _d]),
     "flip_k_sample_velocity_many": (C.c_int, [_d, _d, _d, C.c_int64, C.c_int64, C.c_int64,
                                               C.c_double, C.c_double, C.c_double, C.c_double,

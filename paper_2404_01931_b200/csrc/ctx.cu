@@ -101,7 +101,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
                     c->has_air, c->cell_of_row, c->nbr, c->diagd, c->rhs, c->x, c->r, c->z, c->s,
                     c->q, c->tq, c->precon, c->xtmp, c->u64_scratch, c->lvl, c->lvl_rows,
-                    c->lvl_off, c->lvl_cnt, c->dot_part, c->sc};
+                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->sc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
@@ -196,6 +196,7 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     ALLOC(c->lvl_off, nlev + 1);
     ALLOC(c->lvl_cnt, nlev + 1);
     ALLOC(c->dot_part, dot_tmp_doubles(nc));
+    ALLOC(c->wave_prog, (ny / 8 + 2) * (nz / 8 + 2) + 8);
     ALLOC(c->sc, 1);
     if (cudaMallocHost((void **)&c->sch, sizeof(DevScalars)) != cudaSuccess) {
         set_error("cudaMallocHost failed");
@@ -227,6 +228,11 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
 extern "C" int flip_synchronize(flip_ctx *c) {
     FLIP_CUDA_OK(cudaStreamSynchronize(c->st));
     FLIP_CUDA_OK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int flip_get_stream(flip_ctx *c, void **stream) {
+    *stream = (void *)c->st;
     return 0;
 }
 
@@ -497,6 +503,28 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
 
 extern "C" int flip_step(flip_ctx *c, const flip_step_params *prm, flip_step_report *rep) {
     return flip_run_stages(c, prm, 0, FLIP_NSTAGES - 1, rep);
+}
+
+// Debug/test access to internal device buffers by name (bytes clipped to the
+// buffer size); used by the parity tests to localise mismatches.
+extern "C" int flip_debug_copy(flip_ctx *c, const char *name, void *host, int64_t bytes) {
+    cudaSetDevice(c->device);
+    struct E {
+        const char *n;
+        const void *p;
+        int64_t sz;
+    } tab[] = {{"precon", c->precon, 8 * c->ncells}, {"x", c->x, 8 * c->ncells},
+               {"rhs", c->rhs, 8 * c->ncells},       {"diag", c->diagd, 8 * c->ncells},
+               {"cell_of_row", c->cell_of_row, 4 * c->ncells}, {"rowscan", c->rowscan, 4 * c->ncells},
+               {"nbr", c->nbr, 24 * c->ncells},      {"z", c->z, 8 * c->ncells},
+               {"tq", c->tq, 8 * c->ncells},         {"r", c->r, 8 * c->ncells}};
+    for (auto &e : tab)
+        if (!strcmp(e.n, name)) {
+            TRY(d2h(host, e.p, (size_t)std::min(bytes, e.sz), c->st));
+            return flip_synchronize(c);
+        }
+    set_error(std::string("unknown buffer ") + name);
+    return FLIP_E_ARG;
 }
 
 extern "C" int flip_divergence_field(flip_ctx *c, double *div) {

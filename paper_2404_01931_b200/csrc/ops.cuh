@@ -28,6 +28,7 @@ struct DevScalars {
     double err_value;
     int reseed_changed, new_total;
     int nlevels;
+    int row_lo[3], row_hi[3];           // bounding box of the pressure rows
     int pad;
 };
 
@@ -63,6 +64,7 @@ struct Ctx {
     unsigned long long *u64_scratch = nullptr;
     int *lvl = nullptr, *lvl_rows = nullptr, *lvl_off = nullptr, *lvl_cnt = nullptr;
     double *dot_part = nullptr;
+    int *wave_prog = nullptr;    // wavefront tile progress counters + ticket
     DevScalars *sc = nullptr;    // device
     DevScalars *sch = nullptr;   // pinned host mirror
     cudaEvent_t ev[FLIP_NSTAGES + 1]{};

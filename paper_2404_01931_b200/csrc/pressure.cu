@@ -16,9 +16,13 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "ops.cuh"
+#include "wavefront.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -134,10 +138,11 @@ __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
                                 const double *__restrict__ u, const double *__restrict__ v,
                                 const double *__restrict__ w, int *__restrict__ nbr, int64_t ldn,
                                 double *__restrict__ diag, double *__restrict__ rhs,
-                                unsigned long long *rhsmax) {
+                                unsigned long long *rhsmax, DevScalars *scw) {
     int n = sc->nrows;
     int64_t sxy = (int64_t)d.nx * d.ny;
     double m = 0.0;
+    int lo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, hi[3] = {-1, -1, -1};
     for (int64_t r = gtid(); r < n; r += gstride()) {
         int64_t c = cell_of_row[r];
         int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
@@ -171,9 +176,30 @@ __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
         double rh = -div;
         rhs[r] = rh;
         m = fmax(m, fabs(rh));
+        lo[0] = min(lo[0], i); hi[0] = max(hi[0], i);
+        lo[1] = min(lo[1], j); hi[1] = max(hi[1], j);
+        lo[2] = min(lo[2], k); hi[2] = max(hi[2], k);
     }
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(rhsmax, m);
+    // bounding box of the rows (wavefront geometry)
+    for (int a = 0; a < 3; a++) {
+        for (int o = 16; o; o >>= 1) {
+            lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+        if ((threadIdx.x & 31) == 0 && hi[a] >= 0) {
+            atomicMin(&scw->row_lo[a], lo[a]);
+            atomicMax(&scw->row_hi[a], hi[a]);
+        }
+    }
+}
+
+__global__ void k_bbox_reset(DevScalars *sc) {
+    for (int a = 0; a < 3; a++) {
+        sc->row_lo[a] = 0x7fffffff;
+        sc->row_hi[a] = -1;
+    }
 }
 
 // pressure_field (pressure.py:49-53): dense p, solution on rows, 0 elsewhere.
@@ -747,23 +773,50 @@ static void sweep(const SysView &S, const Levels &L, int reverse, const double *
     (*launches)++;
 }
 
-// Levels for the three sweep kinds: fwd (MIC build / forward), bwd (MIC
-// backward, with reverse flag) and gs.  For assembled systems all three are
-// the geometric hyperplanes (bwd = fwd reversed).
+// How the sequential sweeps are scheduled: for assembled systems the
+// pipelined tile wavefront (wavefront.cu); for arbitrary neighbour tables
+// (plugin API) level-scheduled cooperative sweeps over relaxed levels.
 struct SweepLevels {
     const Levels *fwd, *bwd, *gs;
     int bwd_reverse;
+    const WaveArgs *wave;  // non-null: use the pipelined wavefront
 };
+
+template <int MODE>
+static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src, double *dst,
+                     const double *precon, DevScalars *sc, cudaStream_t st, int64_t *launches) {
+    if (LV.wave) {
+        WaveArgs A = *LV.wave;
+        A.src = src;
+        A.dst = dst;
+        A.precon = precon;
+        A.sc = sc;
+        int ntiles = A.geom.TB * A.geom.TC;
+        cudaMemsetAsync(A.progress, 0, sizeof(int) * (ntiles + 1), st);  // progress + ticket
+        cudaError_t e = launch_wave(MODE, A, st);
+        if (e != cudaSuccess) set_error(std::string("wavefront launch: ") + cudaGetErrorString(e));
+        static const bool dbg = getenv("FLIPB200_DEBUG_SYNC") != nullptr;
+        if (dbg) {
+            cudaError_t e2 = cudaStreamSynchronize(st);
+            fprintf(stderr, "wave mode %d tiles %d nsteps %d launch=%s sync=%s\n", MODE, ntiles,
+                    A.geom.nsteps, cudaGetErrorString(e), cudaGetErrorString(e2));
+        }
+        (*launches)++;
+        return;
+    }
+    const Levels &L = MODE == SW_GS ? *LV.gs : (MODE == SW_MIC_BWD ? *LV.bwd : *LV.fwd);
+    sweep<MODE>(S, L, MODE == SW_MIC_BWD ? LV.bwd_reverse : 0, src, dst, precon, sc, 1, st,
+                launches);
+}
 
 // z = M^-1 r for the selected preconditioner (pressure.py:284-300).
 static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                      const SweepLevels &LV, const double *r, double *z, DevScalars *sc,
                      cudaStream_t st, int64_t *launches) {
     if (cfg.precond == FLIP_PRECOND_MIC0) {
-        // forward substitution into tq (zero-initialised reads are handled
-        // by the k < r guard), then backward into z
-        sweep<SW_MIC_FWD>(S, *LV.fwd, 0, r, B.tq, B.precon, sc, 1, st, launches);
-        sweep<SW_MIC_BWD>(S, *LV.bwd, LV.bwd_reverse, B.tq, z, B.precon, sc, 1, st, launches);
+        // forward substitution into tq, then backward into z
+        do_sweep<SW_MIC_FWD>(S, LV, r, B.tq, B.precon, sc, st, launches);
+        do_sweep<SW_MIC_BWD>(S, LV, B.tq, z, B.precon, sc, st, launches);
     } else {
         k_precond_diag<<<nblocks(S.n), kThreads, 0, st>>>(
             S.n, r, cfg.precond == FLIP_PRECOND_JACOBI ? B.precon : nullptr, z, sc, 1);
@@ -792,7 +845,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     int every = cfg.check_every > 0 ? cfg.check_every : (relax ? 64 : 8);
     if (n > 0 && !relax) {
         if (cfg.precond == FLIP_PRECOND_MIC0)
-            sweep<SW_MIC_BUILD>(S, *LV.fwd, 0, nullptr, B.precon, nullptr, sc, 1, st, launches);
+            do_sweep<SW_MIC_BUILD>(S, LV, nullptr, B.precon, nullptr, sc, st, launches);
         else if (cfg.precond == FLIP_PRECOND_JACOBI) {
             k_inv_diag<<<nblocks(n), kThreads, 0, st>>>(n, S.diag, S.scale, B.precon);
             (*launches)++;
@@ -823,7 +876,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                     *launches += 2;
                 } else {
                     if (cfg.solver == FLIP_SOLVER_GS) {
-                        sweep<SW_GS>(S, *LV.gs, 0, nullptr, B.x, nullptr, sc, 1, st, launches);
+                        do_sweep<SW_GS>(S, LV, nullptr, B.x, nullptr, sc, st, launches);
                     } else {
                         k_gs_rows<<<nblocks(cfg.red ? cfg.nred : n), kThreads, 0, st>>>(
                             S, cfg.red, cfg.nred, 0, cfg.d, B.x, sc, 1);
@@ -872,9 +925,10 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     IsRowIn in{c.label, c.parent, c.has_air};
     exclusive_scan(in, nc, c.rowscan, &c.sc->nrows, c.scan_tmp, st);
     k_rows_compact<<<nblocks(nc), kThreads, 0, st>>>(in, nc, c.rowscan, c.isrow, c.cell_of_row, c.sc);
+    k_bbox_reset<<<1, 1, 0, st>>>(c.sc);
     k_assemble_rows<<<nblocks(nc), kThreads, 0, st>>>(c.d, c.label, c.isrow, c.rowscan,
                                                       c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr, nc,
-                                                      c.diagd, c.rhs, &c.sc->rhsmax_bits);
+                                                      c.diagd, c.rhs, &c.sc->rhsmax_bits, c.sc);
     c.launches += 8;
     cudaMemcpyAsync(c.sch, c.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
     FLIP_CUDA_OK(cudaStreamSynchronize(st));
@@ -885,10 +939,31 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     // scale = dt / (rho * dtau**2) (pressure.py:164), same IEEE division as the reference
     double scale = dt / prm.rho_dtau2_h;
     SysView S{n, c.cell_of_row, c.nbr, nc, c.diagd, c.rhs, scale};
-    bool need_levels = prm.solver == FLIP_SOLVER_GS ||
+    // sequential sweeps (GS, MIC(0)) run as the pipelined wavefront over the
+    // rows' bounding box; FLIPB200_LEVEL_SWEEPS=1 selects the level-scheduled
+    // cooperative fallback (same results, used to cross-check)
+    static const bool level_sweeps = getenv("FLIPB200_LEVEL_SWEEPS") != nullptr;
+    bool need_sweeps = prm.solver == FLIP_SOLVER_GS ||
                        (prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MIC0);
     Levels L{c.lvl, c.lvl_cnt, c.lvl_off, c.lvl_rows, &c.sc->nlevels, 0};
-    if (need_levels && n > 0) {
+    WaveArgs W{};
+    bool use_wave = need_sweeps && n > 0 && !level_sweeps;
+    if (use_wave) {
+        W.d = c.d;
+        W.geom = wave_geom(c.sch->row_lo, c.sch->row_hi);
+        W.rowscan = c.rowscan;
+        W.cell_of_row = c.cell_of_row;
+        W.nbr = c.nbr;
+        W.ldn = nc;
+        W.diag = c.diagd;
+        W.rhs = c.rhs;
+        W.scale = scale;
+        W.tau = 0.97;   // pressure.py:288
+        W.sigma = 0.25;
+        W.progress = c.wave_prog;
+        W.pub = wave_pub();
+        W.ticket = c.wave_prog + W.geom.TB * W.geom.TC;
+    } else if (need_sweeps && n > 0) {
         int maxl = c.d.nx + c.d.ny + c.d.nz - 2;
         cudaMemsetAsync(c.lvl_cnt, 0, sizeof(int) * (maxl + 1), st);
         k_lvl_geom<<<nblocks(n), kThreads, 0, st>>>(c.cell_of_row, n, c.d, c.lvl, c.lvl_cnt);
@@ -896,7 +971,7 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         k_set_nlevels<<<1, 1, 0, st>>>(c.sc, maxl);
         c.launches += 2;
     }
-    SweepLevels LV{&L, &L, &L, 1};
+    SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr};
     SolveCfg cfg{prm.solver, prm.precond, prm.max_iters, prm.tol, prm.solver_check_every, nullptr,
                  nullptr, nullptr, 0, 0, c.d};
     SolveBufs B{c.x, c.r, c.z, c.s, c.q, c.tq, c.precon, c.xtmp, c.dot_part, c.scan_tmp,
@@ -1216,7 +1291,7 @@ extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, con
     }
     if (n > 0 && solver == FLIP_SOLVER_GS)
         if (int rc = generic_levels(ar, V, 2, Lg, S.st, scan_tmp)) return rc;
-    SweepLevels LV{&Lf, &Lb, &Lg, 0};
+    SweepLevels LV{&Lf, &Lb, &Lg, 0, nullptr};
     SolveCfg cfg{solver, precond, max_iters, tol, 0, nullptr, red, black, nred, nblack, Dims{}};
     SolveBufs B{ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),
                 ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),

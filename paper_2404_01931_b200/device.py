@@ -54,6 +54,11 @@ class Device:
         self.version += 1
         self._cache.clear()
 
+    def stream_ptr(self) -> int:
+        sp = C.c_void_p()
+        check(LIB.flip_get_stream(self.ctx, C.byref(sp)))
+        return int(sp.value or 0)
+
     # -- grid --------------------------------------------------------------
     def grid_array(self, name: str) -> np.ndarray:
         key = ("grid", name)
@@ -179,6 +184,12 @@ class Device:
         rc = LIB.flip_run_stages(self.ctx, C.byref(params), int(first), int(last), C.byref(rep))
         self.bump()
         return rc, rep
+
+    def debug_buffer(self, name: str, count: int, dtype=np.float64) -> np.ndarray:
+        out = np.empty(count, dtype=dtype)
+        check(LIB.flip_debug_copy(self.ctx, name.encode(), out.ctypes.data_as(C.c_void_p),
+                                  out.nbytes))
+        return out
 
     def divergence_field(self) -> np.ndarray:
         out = np.empty(self.dims.ncells)
