@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""FLIP timestep benchmark (BASELINE.json: particle-steps/s and ms per step
+at 256^3, dam-break, 8 particles/cell, PCG + MIC(0)).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0.  A "step" is one full flipsim.sim.step() (all ten
+stages) of the dam-break scene at --res (default 256).  The scene comes from
+the reference's own scene builder restated on the device (synthetic, seed 0).
+
+* value     particle-steps/s = sum over timed steps of the particle count
+            entering the step / device time (CUDA events on the library's
+            stream, warm state resident in HBM; max over ranks).
+* e2e       the same metric through the C ABI with HOST buffers: every step
+            uploads particles + labels from pinned host memory, steps, and
+            downloads the particles.
+* roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_sweep,
+            ~90% of the step): algorithmic bytes (3 x 8 B per row) over the
+            measured per-launch time (CUDA events bracketing each launch).
+* cpu_baseline  the oracle (C restatement of the reference step, all host
+            threads) on a bounded sample of the same workload.
+* --impl reference  times the oracle port as the reference arm (the Python
+            reference cannot travel to the GPU box; oracle/ is its bit-exact
+            C restatement, pinned by tests/).
+
+Multi-GPU (torchrun, one process per GPU): until the z-slab decomposition
+lands every rank runs an independent replica ("scaling": "weak").
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+BASE_METRIC = "particle-steps/sec and ms/FLIP step at 256^3 (1/2/4/8 B200) + HBM roofline %"
+UNIT = "particle-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--res", type=int, default=256)
+    ap.add_argument("--scene", default="dam-break")
+    ap.add_argument("--solver", default="pcg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args) -> dict:
+    prec = "MIC(0)-PCG, cap 100" if args.solver == "pcg" else f"{args.solver}, cap 2000"
+    return {"workload": f"{args.scene} {args.res}^3, density 2 (8 particles/cell), {prec}, "
+                        f"tol 1e-6, flip 0.95, seed 0",
+            "res": args.res, "scene": args.scene, "solver": args.solver,
+            "l2_policy": "inputs larger than L2 (particle state >= 1.2 GB per step)"}
+
+
+# ------------------------------------------------------------- clocks -----
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = f"/tmp/flipb200_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7 or f[0] != str(self.idx):
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- oracle -----
+def oracle_sample(args, steps: int, warm: int, threads: int):
+    """Oracle (C restatement of flipsim.sim.step) on the same scene: returns
+    (particle-steps/s, seconds per step, detail)."""
+    sys.path.insert(0, os.path.join(HERE, "oracle"))
+    import oracle as O
+    O.build()
+    O.set_threads(threads)
+    spec = O.Spec(name=args.scene, res=args.res, solver=args.solver)
+    t0 = time.perf_counter()
+    st = O.make_scene(spec, rng_seed=0)
+    setup = time.perf_counter() - t0
+    for _ in range(warm):
+        O.step(st, spec)
+    tot_n, tot_t = 0, 0.0
+    for _ in range(steps):
+        n_in = st.n
+        t0 = time.perf_counter()
+        O.step(st, spec)
+        tot_t += time.perf_counter() - t0
+        tot_n += n_in
+    return tot_n / tot_t, tot_t / max(steps, 1), {"setup_s": round(setup, 2)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # bounded: full 256^3 steps take seconds on the host; cap the sample so
+    # the whole arm finishes in a few minutes
+    steps = max(1, min(args.steps, 3))
+    warm = max(1, min(args.warmup, 1))
+    v, sps, det = oracle_sample(args, steps, warm, threads)
+    sample = (f"{steps} full {args.res}^3 oracle steps after {warm} warm-up step(s) "
+              f"(requested K={args.steps}, W={args.warmup}; capped for time), "
+              f"{threads} OpenMP threads, setup {det['setup_s']} s excluded")
+    line = {"metric": BASE_METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": sps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference scene builder, seed 0)", "config": workload(args),
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- ours -----
+def load_traffic():
+    p = os.path.join(HERE, "profiles", "roofline_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def measured_peak():
+    try:
+        return float(json.load(open(os.path.join(HERE, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def run_ours(args):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+
+    import paper_2404_01931_b200 as P
+    from paper_2404_01931_b200 import _lib
+    from paper_2404_01931_b200._lib import LIB, check
+
+    spec = P.SceneSpec(name=args.scene, res=args.res, solver=args.solver)
+    st = P.make_scene(spec, rng_seed=0, device=local)
+    dev = st.device
+    n0 = st.particles.count
+    warm = max(3, args.warmup)
+    for _ in range(warm):
+        P.step(st, spec)
+    stream = torch.cuda.ExternalStream(dev.stream_ptr(), device=local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---------------- device-resident timed region ----------------
+    clocks = ClockSampler(local)
+    check(LIB.flip_set_probe(dev.ctx, 1))
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    parts = 0
+    launches = 0
+    stage = {}
+    iters = []
+    for _ in range(args.steps):
+        parts += st.particles.count
+        rep = P.step(st, spec)
+        launches += rep.gpu_launches
+        iters.append(rep.solver_iterations)
+        for k, v in rep.timings.as_dict().items():
+            stage[k] = stage.get(k, 0.0) + v
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    pms, plaunch, pbytes = C.c_double(0), C.c_int64(0), C.c_double(0)
+    check(LIB.flip_get_probe(dev.ctx, C.byref(pms), C.byref(plaunch), C.byref(pbytes)))
+    check(LIB.flip_set_probe(dev.ctx, 0))
+    total_parts = parts
+    ms_max = ms
+    if dist is not None:
+        t = torch.tensor([ms, float(parts)], device=f"cuda:{local}", dtype=torch.float64)
+        tm = t.clone()
+        dist.all_reduce(tm[0:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
+        ms_max, total_parts = float(tm[0]), float(t[1])
+    value = total_parts / (ms_max / 1e3)
+
+    # ---------------- end to end through the C ABI (host buffers) ----------
+    e2e = None
+    if not args.no_e2e:
+        # pinned host buffers with headroom for the per-step reseed growth
+        cap = min(int(dev.count() * 1.25) + 4096, 12 * dev.dims.ncells)
+        host = [torch.empty(cap, dtype=torch.float64, pin_memory=True) for _ in range(6)]
+        hv = [h.numpy() for h in host]
+        lab = torch.empty(dev.dims.ncells, dtype=torch.uint8, pin_memory=True).numpy()
+        lab[:] = st.grid.label
+        n = dev.count()
+        check(LIB.flip_get_particles(dev.ctx, *[a.ctypes.data_as(_lib._d) for a in hv]))
+        params = P.sim._params(spec, dev.dims.dtau, 0)
+        repc = _lib.StepReportC()
+        h2d = d2h = 0
+        e2e_steps = args.steps
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_parts = 0
+        for k in range(e2e_steps):
+            # step inputs from pinned host memory
+            check(LIB.flip_set_particles(dev.ctx, n, *[a.ctypes.data_as(_lib._d) for a in hv]))
+            check(LIB.flip_set_grid(dev.ctx, None, None, None, None,
+                                    lab.ctypes.data_as(_lib._u8)))
+            h2d += 48 * n + lab.size
+            params.reseed_seed = P.rng.derive_seed(st.rng_seed, st.step_count + 1)
+            rc = LIB.flip_step(dev.ctx, C.byref(params), C.byref(repc))
+            check(rc)
+            st.step_count += 1
+            e2e_parts += n
+            n = int(repc.particle_count)
+            if n > cap:
+                raise RuntimeError("e2e host buffers too small")
+            # result back to pinned host memory
+            check(LIB.flip_get_particles(dev.ctx, *[a.ctypes.data_as(_lib._d) for a in hv]))
+            d2h += 48 * n
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        dev.bump()
+        w = torch.tensor([wall, float(e2e_parts)], dtype=torch.float64, device=f"cuda:{local}")
+        if dist is not None:
+            wm = w.clone()
+            dist.all_reduce(wm[0:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(w[1:2], op=dist.ReduceOp.SUM)
+            w[0] = wm[0]
+        e2e = {"value": float(w[1]) / float(w[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d // e2e_steps), "d2h_bytes_per_step": int(d2h // e2e_steps),
+               "timing": "wall clock around K synchronous C-ABI steps incl. pinned H2D/D2H"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel ----------------
+    peak, peak_kind = measured_peak()
+    roof = None
+    if plaunch.value > 0:
+        avg_ms = pms.value / plaunch.value
+        alg = pbytes.value / plaunch.value
+        achieved = alg / (avg_ms / 1e3) / 1e9
+        tr = load_traffic()
+        roof = {"bound": "hbm", "kernel": "k_mic_sweep (MIC(0) substitution wavefront)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
+                "avg_launch_ms": avg_ms, "launches_timed": int(plaunch.value),
+                "share_of_step": pms.value / ms,
+                "traffic": (tr or {}).get("k_mic_sweep_dram_bytes_per_launch"),
+                "note": "latency-bound dependency wavefront (see DESIGN.md); "
+                        "frac is of the HBM copy peak"}
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        try:
+            threads = os.cpu_count() or 1
+            v, sps, det = oracle_sample(args, 1, 1, threads)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"1 full {args.res}^3 oracle step after 1 warm-up step, "
+                             f"{threads} OpenMP threads (setup {det['setup_s']} s excluded)"}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    line = {"metric": BASE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": warm, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference dam-break scene builder on the device, seed 0)",
+            "config": dict(workload(args), particles_initial=n0,
+                           parallelism="replicas" if world > 1 else "single"),
+            "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+            "cpu_baseline": cpu,
+            "detail": {"stage_ms_mean": {k: v / args.steps for k, v in stage.items()},
+                       "solver_iterations": iters,
+                       "particles_final": st.particles.count}}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

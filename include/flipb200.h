@@ -172,6 +172,12 @@ int flip_run_stages(flip_ctx *ctx, const flip_step_params *params, int32_t first
  * host div[ncells]; total_energy sums (sim.py:303-315) with numpy pairwise
  * order: ke2 = sum(vx^2+vy^2+vz^2), pe = sum(py - floor_y). */
 int flip_divergence_field(flip_ctx *ctx, double *div);
+/* Timing probe (bench roofline evidence): kind 1 brackets every MIC(0)
+ * substitution sweep launch with CUDA events on the ctx stream; get returns
+ * the summed duration, the number of bracketed launches (<= 1024 per
+ * flip_set_probe) and their algorithmic bytes (3 x 8 B per row). */
+int flip_set_probe(flip_ctx *ctx, int32_t kind);
+int flip_get_probe(flip_ctx *ctx, double *total_ms, int64_t *launches, double *alg_bytes);
 /* Test hook: copy an internal device buffer ("precon", "x", "rhs", "diag",
  * "cell_of_row", "rowscan", "nbr", "z", "tq", "r") to host. */
 int flip_debug_copy(flip_ctx *ctx, const char *name, void *host, int64_t bytes);

@@ -115,6 +115,8 @@ _SIGNATURES = {
                                   C.POINTER(StepReportC)]),
     "flip_divergence_field": (C.c_int, [_vp, _d]),
     "flip_debug_copy": (C.c_int, [_vp, C.c_char_p, _vp, C.c_int64]),
+    "flip_set_probe": (C.c_int, [_vp, C.c_int32]),
+    "flip_get_probe": (C.c_int, [_vp, _d, _i64, _d]),
     "flip_energy_sums": (C.c_int, [_vp, C.c_double, _d, _d]),
     "flip_k_sample_velocity_many": (C.c_int, [_d, _d, _d, C.c_int64, C.c_int64, C.c_int64,
                                               C.c_double, C.c_double, C.c_double, C.c_double,

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "ops.cuh"
+#include "wavefront.cuh"
 
 namespace flip {
 
@@ -101,11 +102,13 @@ extern "C" void flip_destroy(flip_ctx *c) {
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
                     c->has_air, c->cell_of_row, c->nbr, c->diagd, c->rhs, c->x, c->r, c->z, c->s,
                     c->q, c->tq, c->precon, c->xtmp, c->u64_scratch, c->lvl, c->lvl_rows,
-                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->sc};
+                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->sc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
     for (auto &e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : c->probe.ev)
         if (e) cudaEventDestroy(e);
     if (c->st) cudaStreamDestroy(c->st);
     delete c;
@@ -196,7 +199,10 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     ALLOC(c->lvl_off, nlev + 1);
     ALLOC(c->lvl_cnt, nlev + 1);
     ALLOC(c->dot_part, dot_tmp_doubles(nc));
-    ALLOC(c->wave_prog, (ny / 8 + 2) * (nz / 8 + 2) + 8);
+    ALLOC(c->wave_prog, 8);
+    ALLOC(c->wave_halo, wave_halo_doubles(nx, ny, nz));
+    ALLOC(c->cflags, nc);
+    ALLOC(c->wave_trace, 4 * 4096 + 1024);
     ALLOC(c->sc, 1);
     if (cudaMallocHost((void **)&c->sch, sizeof(DevScalars)) != cudaSuccess) {
         set_error("cudaMallocHost failed");
@@ -517,7 +523,8 @@ extern "C" int flip_debug_copy(flip_ctx *c, const char *name, void *host, int64_
                {"rhs", c->rhs, 8 * c->ncells},       {"diag", c->diagd, 8 * c->ncells},
                {"cell_of_row", c->cell_of_row, 4 * c->ncells}, {"rowscan", c->rowscan, 4 * c->ncells},
                {"nbr", c->nbr, 24 * c->ncells},      {"z", c->z, 8 * c->ncells},
-               {"tq", c->tq, 8 * c->ncells},         {"r", c->r, 8 * c->ncells}};
+               {"tq", c->tq, 8 * c->ncells},         {"r", c->r, 8 * c->ncells},
+               {"wave_trace", c->wave_trace, 8 * (4 * 4096 + 1024)}};
     for (auto &e : tab)
         if (!strcmp(e.n, name)) {
             TRY(d2h(host, e.p, (size_t)std::min(bytes, e.sz), c->st));
@@ -525,6 +532,33 @@ extern "C" int flip_debug_copy(flip_ctx *c, const char *name, void *host, int64_
         }
     set_error(std::string("unknown buffer ") + name);
     return FLIP_E_ARG;
+}
+
+extern "C" int flip_set_probe(flip_ctx *c, int32_t kind) {
+    cudaSetDevice(c->device);
+    if (kind && !c->probe.ev[0])
+        for (auto &e : c->probe.ev) FLIP_CUDA_OK(cudaEventCreate(&e));
+    c->probe.kind = kind;
+    c->probe.used = 0;
+    c->probe.bytes = 0.0;
+    c->probe.launches = 0;
+    return 0;
+}
+
+extern "C" int flip_get_probe(flip_ctx *c, double *total_ms, int64_t *launches, double *bytes) {
+    cudaSetDevice(c->device);
+    TRY(flip_synchronize(c));
+    double tot = 0.0;
+    for (int k = 0; k < c->probe.used; k++) {
+        float ms = 0.f;
+        FLIP_CUDA_OK(cudaEventElapsedTime(&ms, c->probe.ev[2 * k], c->probe.ev[2 * k + 1]));
+        tot += ms;
+    }
+    *total_ms = tot;
+    *launches = c->probe.used;
+    *bytes = c->probe.used == c->probe.launches ? c->probe.bytes
+                                                : c->probe.bytes * c->probe.used / c->probe.launches;
+    return 0;
 }
 
 extern "C" int flip_divergence_field(flip_ctx *c, double *div) {

@@ -32,6 +32,16 @@ struct DevScalars {
     int pad;
 };
 
+// CUDA-event bracketing of one kernel class (bench roofline evidence).
+struct Probe {
+    int kind = 0;              // 0 off, 1 MIC(0) substitution sweeps
+    int used = 0;
+    static constexpr int kMax = 1024;
+    cudaEvent_t ev[2 * kMax]{};
+    double bytes = 0.0;        // algorithmic bytes of the bracketed launches
+    int64_t launches = 0;
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;
@@ -64,11 +74,15 @@ struct Ctx {
     unsigned long long *u64_scratch = nullptr;
     int *lvl = nullptr, *lvl_rows = nullptr, *lvl_off = nullptr, *lvl_cnt = nullptr;
     double *dot_part = nullptr;
-    int *wave_prog = nullptr;    // wavefront tile progress counters + ticket
+    int *wave_prog = nullptr;    // wavefront tile ticket
+    double *wave_halo = nullptr; // wavefront tile-face halo buffers
+    unsigned long long *wave_trace = nullptr;  // optional per-tile timing
+    unsigned char *cflags = nullptr;  // per-cell sweep flags
     DevScalars *sc = nullptr;    // device
     DevScalars *sch = nullptr;   // pinned host mirror
     cudaEvent_t ev[FLIP_NSTAGES + 1]{};
     int64_t launches = 0;
+    Probe probe;
     int known_valid = 0;
     int keys_valid = 0;   // keys_sorted matches the current binned particles
 };

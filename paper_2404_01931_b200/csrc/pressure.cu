@@ -780,6 +780,7 @@ struct SweepLevels {
     const Levels *fwd, *bwd, *gs;
     int bwd_reverse;
     const WaveArgs *wave;  // non-null: use the pipelined wavefront
+    Probe *probe;          // optional event bracketing of the MIC substitutions
 };
 
 template <int MODE>
@@ -791,17 +792,19 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
         A.dst = dst;
         A.precon = precon;
         A.sc = sc;
-        int ntiles = A.geom.TB * A.geom.TC;
-        cudaMemsetAsync(A.progress, 0, sizeof(int) * (ntiles + 1), st);  // progress + ticket
+        Probe *pb = LV.probe;
+        bool probed = pb && pb->kind == 1 && (MODE == SW_MIC_FWD || MODE == SW_MIC_BWD) &&
+                      pb->used < Probe::kMax;
+        if (probed) cudaEventRecord(pb->ev[2 * pb->used], st);
         cudaError_t e = launch_wave(MODE, A, st);
-        if (e != cudaSuccess) set_error(std::string("wavefront launch: ") + cudaGetErrorString(e));
-        static const bool dbg = getenv("FLIPB200_DEBUG_SYNC") != nullptr;
-        if (dbg) {
-            cudaError_t e2 = cudaStreamSynchronize(st);
-            fprintf(stderr, "wave mode %d tiles %d nsteps %d launch=%s sync=%s\n", MODE, ntiles,
-                    A.geom.nsteps, cudaGetErrorString(e), cudaGetErrorString(e2));
+        if (probed) {
+            cudaEventRecord(pb->ev[2 * pb->used + 1], st);
+            pb->used++;
+            pb->launches++;
+            pb->bytes += 24.0 * (double)A.n;  // src + precon read, dst written: 3 x 8 B per row
         }
-        (*launches)++;
+        if (e != cudaSuccess) set_error(std::string("wavefront launch: ") + cudaGetErrorString(e));
+        *launches += 2;
         return;
     }
     const Levels &L = MODE == SW_GS ? *LV.gs : (MODE == SW_MIC_BWD ? *LV.bwd : *LV.fwd);
@@ -876,7 +879,11 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                     *launches += 2;
                 } else {
                     if (cfg.solver == FLIP_SOLVER_GS) {
-                        do_sweep<SW_GS>(S, LV, nullptr, B.x, nullptr, sc, st, launches);
+                        if (LV.wave) {  // out of place: old x in, new x out, copied back below
+                            do_sweep<SW_GS>(S, LV, B.x, B.xtmp, nullptr, sc, st, launches);
+                        } else {
+                            do_sweep<SW_GS>(S, LV, nullptr, B.x, nullptr, sc, st, launches);
+                        }
                     } else {
                         k_gs_rows<<<nblocks(cfg.red ? cfg.nred : n), kThreads, 0, st>>>(
                             S, cfg.red, cfg.nred, 0, cfg.d, B.x, sc, 1);
@@ -884,8 +891,10 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                             S, cfg.black, cfg.nblack, 1, cfg.d, B.x, sc, 1);
                         *launches += 2;
                     }
-                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.x, nullptr, S.rhs, &sc->res_bits,
-                                                              nullptr, sc, 1);
+                    bool gs_oop = cfg.solver == FLIP_SOLVER_GS && LV.wave;
+                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, gs_oop ? B.xtmp : B.x, nullptr,
+                                                              S.rhs, &sc->res_bits,
+                                                              gs_oop ? B.x : nullptr, sc, 1);
                     (*launches)++;
                 }
                 k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
@@ -952,17 +961,19 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         W.d = c.d;
         W.geom = wave_geom(c.sch->row_lo, c.sch->row_hi);
         W.rowscan = c.rowscan;
-        W.cell_of_row = c.cell_of_row;
-        W.nbr = c.nbr;
-        W.ldn = nc;
+        W.cflags = c.cflags;
+        W.n = n;
         W.diag = c.diagd;
         W.rhs = c.rhs;
         W.scale = scale;
         W.tau = 0.97;   // pressure.py:288
         W.sigma = 0.25;
-        W.progress = c.wave_prog;
-        W.pub = wave_pub();
-        W.ticket = c.wave_prog + W.geom.TB * W.geom.TC;
+        W.halo_y = c.wave_halo;
+        W.halo_z = c.wave_halo + (int64_t)W.geom.TB * W.geom.TC * W.geom.tz * W.geom.ispan_pad;
+        W.ticket = c.wave_prog;
+        W.trace = getenv("FLIPB200_WAVE_TRACE") ? c.wave_trace : nullptr;
+        launch_cell_flags(c.d, c.isrow, c.cflags, st);
+        c.launches++;
     } else if (need_sweeps && n > 0) {
         int maxl = c.d.nx + c.d.ny + c.d.nz - 2;
         cudaMemsetAsync(c.lvl_cnt, 0, sizeof(int) * (maxl + 1), st);
@@ -971,7 +982,7 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         k_set_nlevels<<<1, 1, 0, st>>>(c.sc, maxl);
         c.launches += 2;
     }
-    SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr};
+    SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr, &c.probe};
     SolveCfg cfg{prm.solver, prm.precond, prm.max_iters, prm.tol, prm.solver_check_every, nullptr,
                  nullptr, nullptr, 0, 0, c.d};
     SolveBufs B{c.x, c.r, c.z, c.s, c.q, c.tq, c.precon, c.xtmp, c.dot_part, c.scan_tmp,
@@ -1291,7 +1302,7 @@ extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, con
     }
     if (n > 0 && solver == FLIP_SOLVER_GS)
         if (int rc = generic_levels(ar, V, 2, Lg, S.st, scan_tmp)) return rc;
-    SweepLevels LV{&Lf, &Lb, &Lg, 0, nullptr};
+    SweepLevels LV{&Lf, &Lb, &Lg, 0, nullptr, nullptr};
     SolveCfg cfg{solver, precond, max_iters, tol, 0, nullptr, red, black, nred, nblack, Dims{}};
     SolveBufs B{ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),
                 ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),
