@@ -102,7 +102,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
                     c->has_air, c->cell_of_row, c->nbr, c->diagd, c->rhs, c->x, c->r, c->z, c->s,
                     c->q, c->tq, c->precon, c->xtmp, c->u64_scratch, c->lvl, c->lvl_rows,
-                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->sc};
+                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->lrow, c->posL, c->laneA, c->laneB, c->laneC, c->laneD, c->sc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
@@ -202,7 +202,14 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     ALLOC(c->wave_prog, 8);
     ALLOC(c->wave_halo, wave_halo_doubles(nx, ny, nz));
     ALLOC(c->cflags, nc);
-    ALLOC(c->wave_trace, 4 * 4096 + 1024);
+    c->lane_cap = lane_entries_max(nx, ny, nz);
+    ALLOC(c->lrow, c->lane_cap);
+    ALLOC(c->posL, nc);
+    ALLOC(c->laneA, c->lane_cap);
+    ALLOC(c->laneB, c->lane_cap);
+    ALLOC(c->laneC, c->lane_cap);
+    ALLOC(c->laneD, c->lane_cap);
+    ALLOC(c->wave_trace, 32768);
     ALLOC(c->sc, 1);
     if (cudaMallocHost((void **)&c->sch, sizeof(DevScalars)) != cudaSuccess) {
         set_error("cudaMallocHost failed");
@@ -524,7 +531,7 @@ extern "C" int flip_debug_copy(flip_ctx *c, const char *name, void *host, int64_
                {"cell_of_row", c->cell_of_row, 4 * c->ncells}, {"rowscan", c->rowscan, 4 * c->ncells},
                {"nbr", c->nbr, 24 * c->ncells},      {"z", c->z, 8 * c->ncells},
                {"tq", c->tq, 8 * c->ncells},         {"r", c->r, 8 * c->ncells},
-               {"wave_trace", c->wave_trace, 8 * (4 * 4096 + 1024)}};
+               {"wave_trace", c->wave_trace, 8 * 32768}};
     for (auto &e : tab)
         if (!strcmp(e.n, name)) {
             TRY(d2h(host, e.p, (size_t)std::min(bytes, e.sz), c->st));

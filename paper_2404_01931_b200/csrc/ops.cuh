@@ -78,6 +78,10 @@ struct Ctx {
     double *wave_halo = nullptr; // wavefront tile-face halo buffers
     unsigned long long *wave_trace = nullptr;  // optional per-tile timing
     unsigned char *cflags = nullptr;  // per-cell sweep flags
+    // lane-major MIC(0) operand layout (wavefront.cu, k_mic_lane)
+    int64_t lane_cap = 0;
+    int *lrow = nullptr, *posL = nullptr;
+    double *laneA = nullptr, *laneB = nullptr, *laneC = nullptr, *laneD = nullptr;
     DevScalars *sc = nullptr;    // device
     DevScalars *sch = nullptr;   // pinned host mirror
     cudaEvent_t ev[FLIP_NSTAGES + 1]{};

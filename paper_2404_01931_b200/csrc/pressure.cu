@@ -776,11 +776,19 @@ static void sweep(const SysView &S, const Levels &L, int reverse, const double *
 // How the sequential sweeps are scheduled: for assembled systems the
 // pipelined tile wavefront (wavefront.cu); for arbitrary neighbour tables
 // (plugin API) level-scheduled cooperative sweeps over relaxed levels.
+// Lane-major layout of the MIC(0) substitution operands (assembled systems).
+struct LaneBufs {
+    LaneArgs args;       // geometry, halos, ticket, scale
+    const int *posL;     // row -> L entry
+    double *rL, *tqL, *zL, *preL;
+};
+
 struct SweepLevels {
     const Levels *fwd, *bwd, *gs;
     int bwd_reverse;
     const WaveArgs *wave;  // non-null: use the pipelined wavefront
     Probe *probe;          // optional event bracketing of the MIC substitutions
+    const LaneBufs *lane;  // non-null: MIC(0) apply through the lane-major kernels
 };
 
 template <int MODE>
@@ -816,7 +824,31 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
 static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                      const SweepLevels &LV, const double *r, double *z, DevScalars *sc,
                      cudaStream_t st, int64_t *launches) {
-    if (cfg.precond == FLIP_PRECOND_MIC0) {
+    if (cfg.precond == FLIP_PRECOND_MIC0 && LV.lane) {
+        // r -> L layout, forward (L), backward (L), back to rows
+        const LaneBufs &Lb = *LV.lane;
+        launch_rows_to_lane(r, Lb.posL, S.n, Lb.rL, sc, st);
+        Probe *pb = LV.probe;
+        for (int rev = 0; rev < 2; rev++) {
+            LaneArgs A = Lb.args;
+            A.src = rev ? Lb.tqL : Lb.rL;
+            A.dst = rev ? Lb.zL : Lb.tqL;
+            A.precon = Lb.preL;
+            A.sc = sc;
+            bool probed = pb && pb->kind == 1 && pb->used < Probe::kMax;
+            if (probed) cudaEventRecord(pb->ev[2 * pb->used], st);
+            cudaError_t e = launch_mic_lane(rev != 0, A, st);
+            if (e != cudaSuccess) set_error(std::string("lane sweep launch: ") + cudaGetErrorString(e));
+            if (probed) {
+                cudaEventRecord(pb->ev[2 * pb->used + 1], st);
+                pb->used++;
+                pb->launches++;
+                pb->bytes += 24.0 * (double)S.n;  // src + precon read, dst written per row
+            }
+        }
+        launch_lane_to_rows(Lb.zL, Lb.posL, S.n, z, sc, st);
+        *launches += 2 * 2 + 2;
+    } else if (cfg.precond == FLIP_PRECOND_MIC0) {
         // forward substitution into tq, then backward into z
         do_sweep<SW_MIC_FWD>(S, LV, r, B.tq, B.precon, sc, st, launches);
         do_sweep<SW_MIC_BWD>(S, LV, B.tq, z, B.precon, sc, st, launches);
@@ -847,8 +879,13 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     }
     int every = cfg.check_every > 0 ? cfg.check_every : (relax ? 64 : 8);
     if (n > 0 && !relax) {
-        if (cfg.precond == FLIP_PRECOND_MIC0)
+        if (cfg.precond == FLIP_PRECOND_MIC0) {
             do_sweep<SW_MIC_BUILD>(S, LV, nullptr, B.precon, nullptr, sc, st, launches);
+            if (LV.lane) {
+                launch_rows_to_lane(B.precon, LV.lane->posL, n, LV.lane->preL, sc, st);
+                (*launches)++;
+            }
+        }
         else if (cfg.precond == FLIP_PRECOND_JACOBI) {
             k_inv_diag<<<nblocks(n), kThreads, 0, st>>>(n, S.diag, S.scale, B.precon);
             (*launches)++;
@@ -982,7 +1019,28 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         k_set_nlevels<<<1, 1, 0, st>>>(c.sc, maxl);
         c.launches += 2;
     }
-    SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr, &c.probe};
+    LaneBufs LB{};
+    static const bool no_lane = getenv("FLIPB200_NO_LANE") != nullptr;
+    bool use_lane = use_wave && prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MIC0 &&
+                    !no_lane && lane_entries(W.geom) <= c.lane_cap;
+    if (use_lane) {
+        LB.args.geom = W.geom;
+        LB.args.halo_y = W.halo_y;
+        LB.args.halo_z = W.halo_z;
+        LB.args.scale = scale;
+        LB.args.ticket = W.ticket;
+        LB.args.trace = getenv("FLIPB200_WAVE_TRACE") ? c.wave_trace : nullptr;
+        LB.args.dbg = getenv("FLIPB200_LANE_DBG") ? atoi(getenv("FLIPB200_LANE_DBG")) : 0;
+        LB.args.mode = getenv("FLIPB200_LANE_MODE") ? atoi(getenv("FLIPB200_LANE_MODE")) : 0;
+        LB.posL = c.posL;
+        LB.rL = c.laneA;
+        LB.tqL = c.laneB;
+        LB.zL = c.laneC;
+        LB.preL = c.laneD;
+        launch_lane_map(W.geom, c.d, c.isrow, c.rowscan, c.lrow, c.posL, c.laneA, c.laneB, st);
+        c.launches++;
+    }
+    SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr, &c.probe, use_lane ? &LB : nullptr};
     SolveCfg cfg{prm.solver, prm.precond, prm.max_iters, prm.tol, prm.solver_check_every, nullptr,
                  nullptr, nullptr, 0, 0, c.d};
     SolveBufs B{c.x, c.r, c.z, c.s, c.q, c.tq, c.precon, c.xtmp, c.dot_part, c.scan_tmp,
@@ -1302,7 +1360,7 @@ extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, con
     }
     if (n > 0 && solver == FLIP_SOLVER_GS)
         if (int rc = generic_levels(ar, V, 2, Lg, S.st, scan_tmp)) return rc;
-    SweepLevels LV{&Lf, &Lb, &Lg, 0, nullptr, nullptr};
+    SweepLevels LV{&Lf, &Lb, &Lg, 0, nullptr, nullptr, nullptr};
     SolveCfg cfg{solver, precond, max_iters, tol, 0, nullptr, red, black, nred, nblack, Dims{}};
     SolveBufs B{ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),
                 ar.get<double>(n), ar.get<double>(n), ar.get<double>(n), ar.get<double>(n),

@@ -52,6 +52,7 @@ __device__ __forceinline__ void ticket_tile(int t, int TB, int TC, int &b, int &
 }
 
 constexpr int U = 4;  // steps per unrolled round (prefetch distance U / 2U)
+constexpr int LANE_NB = 3;  // k_mic_lane2 operand chunk ring depth
 
 template <int MODE, int TY, int TZ>
 __global__ void __launch_bounds__(TY *TZ) k_wave(WaveArgs A) {
@@ -457,6 +458,445 @@ __global__ void __launch_bounds__(TY *TZ) k_mic_sweep(WaveArgs A) {
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// Lane-major MIC(0) substitution (the production sweep).  Operands live in a
+// skewed tile-major layout L[tile][step][lane]: entry (t, s, p) is the cell
+// lane p of tile t visits at forward step s (i = ilo + s - jj - kk).  A CTA
+// step therefore reads/writes one contiguous TY*TZ*8-byte block per array
+// (fully coalesced), instead of one cache line per lane.  The backward sweep
+// visits the same entries in reverse step order with the same lanes
+// (s' = nsteps-1-s), so one layout serves both sweeps.  Non-row cells hold
+// the ABSENT marker in the input vector: row-ness comes with the data.
+template <bool REV, int TY, int TZ>
+__global__ void __launch_bounds__(TY *TZ) k_mic_lane(LaneArgs A) {
+    constexpr int TP = TY * TZ;
+    constexpr int HR = 2 * U;
+    __shared__ double sval[2][TZ][TY];
+    __shared__ __align__(16) double hyb[TZ][HR];
+    __shared__ __align__(16) double hzb[TY][HR];
+    __shared__ int s_tile;
+    const int p = threadIdx.x, jj = p % TY, kk = p / TY;
+    if (A.sc && A.sc->done) return;
+    const WaveGeom G = A.geom;
+    if (p == 0) s_tile = atomicAdd(A.ticket, 1);
+    __syncthreads();
+    int b, c;
+    ticket_tile(s_tile, G.TB, G.TC, b, c);
+    if (REV) {  // backward: far corner first, same tile partition
+        b = G.TB - 1 - b;
+        c = G.TC - 1 - c;
+    }
+    const int tile = b * G.TC + c;
+    const int nsteps = G.nsteps;
+    const int64_t base = (int64_t)tile * nsteps * TP + p;
+    const double *srcL = A.src + base;
+    const double *preL = A.precon + base;
+    double *dstL = A.dst + base;
+    const int LL = G.ispan_pad;
+    // faces: forward consumes -y/-z and produces +y/+z; backward the reverse
+    double *hy_out = REV ? (jj == 0 ? A.halo_y + ((int64_t)tile * TZ + kk) * LL : nullptr)
+                         : (jj == TY - 1 ? A.halo_y + ((int64_t)tile * TZ + kk) * LL : nullptr);
+    double *hz_out = REV ? (kk == 0 ? A.halo_z + ((int64_t)tile * TY + jj) * LL : nullptr)
+                         : (kk == TZ - 1 ? A.halo_z + ((int64_t)tile * TY + jj) * LL : nullptr);
+    const double *hy_in =
+        REV ? ((jj == TY - 1 && b + 1 < G.TB) ? A.halo_y + ((int64_t)(tile + G.TC) * TZ + kk) * LL : nullptr)
+            : ((jj == 0 && b > 0) ? A.halo_y + ((int64_t)(tile - G.TC) * TZ + kk) * LL : nullptr);
+    const double *hz_in =
+        REV ? ((kk == TZ - 1 && c + 1 < G.TC) ? A.halo_z + ((int64_t)(tile + 1) * TY + jj) * LL : nullptr)
+            : ((kk == 0 && c > 0) ? A.halo_z + ((int64_t)(tile - 1) * TY + jj) * LL : nullptr);
+    const bool y_local = REV ? jj + 1 < TY : jj > 0;
+    const bool z_local = REV ? kk + 1 < TZ : kk > 0;
+    const int yj = REV ? jj + 1 : jj - 1, zk = REV ? kk + 1 : kk - 1;
+    const double absent = __longlong_as_double((long long)WAVE_ABSENT);
+    const int jrow = G.jlo + b * TY + jj, krow = G.klo + c * TZ + kk;
+    const bool valid = jrow <= G.jhi && krow <= G.khi;
+
+    auto lstep = [&](int s) { return REV ? nsteps - 1 - s : s; };  // layout step
+    auto xof = [&](int s) { return lstep(s) - jj - kk; };          // i - ilo
+    double av[U], bv[U];
+    auto load = [&](int s, int u) {
+        int sl = min(lstep(s), nsteps - 1);
+        sl = max(sl, 0);
+        av[u] = srcL[(int64_t)sl * TP];
+        bv[u] = preL[(int64_t)sl * TP];
+        int x = xof(s);
+        bool in = valid && s < nsteps && x >= 0 && x < G.ispan;
+        bool first = in && (((x & 1) == (REV ? 1 : 0)) || x == (REV ? G.ispan - 1 : 0));
+        if (first) {
+            int pb = x & ~1;
+            if (hy_in) cp_async16(&hyb[kk][pb % HR], hy_in + pb);
+            if (hz_in) cp_async16(&hzb[jj][pb % HR], hz_in + pb);
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int u = 0; u < U; u++) load(u, u);
+
+    double pv = absent;
+    const double sc = A.scale;
+    for (int s0 = 0; s0 < nsteps; s0 += U) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int s = s0 + u;
+            if (s >= nsteps) break;  // uniform
+            if (!(A.dbg & 1)) __syncthreads();
+            if (A.trace && tile == 0 && p == 0 && s < 256) A.trace[s] = (unsigned long long)clock64();
+            const int cur = s & 1, prv = cur ^ 1;
+            const double a = (A.dbg & 4) ? 1.0 : av[u], pr = (A.dbg & 4) ? 1.0 : bv[u];
+            const int x = xof(s);
+            double out = absent;
+            if (present(a) && valid && x >= 0 && x < G.ispan) {
+                double yv = absent, zv = absent;
+                if (A.dbg & 8) {
+                } else if (y_local) {
+                    yv = sval[prv][kk][yj];
+                } else if (hy_in) {
+                    cp_async_wait<U - 1>();
+                    yv = hyb[kk][x % HR];
+                    if (is_pending(yv)) yv = poll_ready(hy_in + x);
+                }
+                if (A.dbg & 8) {
+                } else if (z_local) {
+                    zv = sval[prv][zk][jj];
+                } else if (hz_in) {
+                    cp_async_wait<U - 1>();
+                    zv = hzb[jj][x % HR];
+                    if (is_pending(zv)) zv = poll_ready(hz_in + x);
+                }
+                if (!REV) {  // _core.pyx:322-332; publishes scale*precon*q
+                    double t = a;
+                    if (present(pv)) t += pv;
+                    if (present(yv)) t += yv;
+                    if (present(zv)) t += zv;
+                    double q = t * pr;
+                    if (!(A.dbg & 32)) dstL[(int64_t)lstep(s) * TP] = q;
+                    out = (sc * pr) * q;
+                } else {  // _core.pyx:333-346
+                    double t = a;
+                    const double sp = sc * pr;
+                    if (present(pv)) t += sp * pv;
+                    if (present(yv)) t += sp * yv;
+                    if (present(zv)) t += sp * zv;
+                    out = t * pr;
+                    if (!(A.dbg & 32)) dstL[(int64_t)lstep(s) * TP] = out;
+                }
+            }
+            sval[cur][kk][jj] = out;
+            pv = out;
+            if (!(A.dbg & 2) && (hy_out || hz_out) && valid && x >= 0 && x < G.ispan) {
+                if (hy_out) publish(hy_out + x, out);
+                if (hz_out) publish(hz_out + x, out);
+            }
+            if (!(A.dbg & 16)) load(s + U, u);
+        }
+    }
+    cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// ---- bulk-copy (TMA engine, non-tensor) + mbarrier helpers -----------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy, completion counted on *bar (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// k_mic_lane2: warp-specialised lane-major MIC(0) substitution.
+//
+// Warps 0..TP/32-1 compute; one extra helper warp owns every cross-tile
+// transfer, so the compute body is branch-light and never touches a halo.
+// Absent neighbours (not a row, outside the box) are encoded as -0.0: for any
+// t, t + (-0.0) == t bit for bit (IEEE), and in the backward sweep the
+// multiplier scale*precon is strictly positive so (sp * -0.0) == -0.0 too —
+// the reference's "if nb >= 0: t += ..." is reproduced exactly with no test.
+// Shared exchange sval[slot][TZ+2][TY+2]: lane (jj,kk) lives at [kk+1][jj+1];
+// the predecessor tile's face values land in the border row/column, written
+// by the helper one step ahead.
+template <bool REV, int TY, int TZ, int U, int KC>
+__global__ void __launch_bounds__(TY *TZ + 32) k_mic_lane2(LaneArgs A) {
+    constexpr int TP = TY * TZ;
+    static_assert(TY + TZ <= 32, "one helper warp covers both faces");
+    __shared__ double sval[2][TZ + 2][TY + 2];
+    __shared__ int s_tile;
+    const int t = threadIdx.x;
+    if (A.sc && A.sc->done) return;
+    const WaveGeom G = A.geom;
+    unsigned long long t_start = 0;
+    if (t == 0) {
+        s_tile = atomicAdd(A.ticket, 1);
+        if (A.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    }
+    const double nz0 = -0.0;
+    for (int q = t; q < 2 * (TZ + 2) * (TY + 2); q += blockDim.x) (&sval[0][0][0])[q] = nz0;
+    __syncthreads();
+    int b, c;
+    ticket_tile(s_tile, G.TB, G.TC, b, c);
+    if (REV) {
+        b = G.TB - 1 - b;
+        c = G.TC - 1 - c;
+    }
+    const int tile = b * G.TC + c;
+    const int nsteps = G.nsteps;
+    auto lstep = [&](int s) { return REV ? nsteps - 1 - s : s; };
+
+    if (t >= TP) {
+        // ------------------------------ helper warp ------------------------
+        // Halo layout is step-major: face[tile][step][lane] holds the boundary
+        // lane's output at that step.  A consumer at step s needs its
+        // predecessor's step s + D (D = TY-1 across a y face, TZ-1 across a z
+        // face, in both sweep directions), so every publish and every fetch is
+        // one contiguous 16-lane access.
+        const int l = t - TP;
+        // lanes [0,TZ): y face, lane kk; lanes [TZ,TZ+TY): z face, lane jj
+        const bool yface = l < TZ, zface = l >= TZ && l < TZ + TY;
+        const bool active = yface || zface;
+        const int kk = yface ? l : 0, jj = zface ? l - TZ : 0;
+        const int W = yface ? TZ : TY;       // lanes per face row
+        const int D = yface ? TY - 1 : TZ - 1;
+        const double *in = nullptr;
+        double *out = nullptr;
+        int in_row = 0, in_col = 0, out_row = 0, out_col = 0, cons_j = 0, cons_k = 0;
+        if (yface) {
+            cons_j = REV ? TY - 1 : 0;
+            cons_k = kk;
+            const bool has = REV ? b + 1 < G.TB : b > 0;
+            if (has) in = A.halo_y + (int64_t)(REV ? tile + G.TC : tile - G.TC) * nsteps * TZ + kk;
+            out = A.halo_y + (int64_t)tile * nsteps * TZ + kk;
+            in_row = kk + 1;
+            in_col = REV ? TY + 1 : 0;
+            out_row = kk + 1;
+            out_col = (REV ? 0 : TY - 1) + 1;
+        } else if (zface) {
+            cons_j = jj;
+            cons_k = REV ? TZ - 1 : 0;
+            const bool has = REV ? c + 1 < G.TC : c > 0;
+            if (has) in = A.halo_z + (int64_t)(REV ? tile + 1 : tile - 1) * nsteps * TY + jj;
+            out = A.halo_z + (int64_t)tile * nsteps * TY + jj;
+            in_row = REV ? TZ + 1 : 0;
+            in_col = jj + 1;
+            out_row = (REV ? 0 : TZ - 1) + 1;
+            out_col = jj + 1;
+        }
+        // a consumer lane outside the box never computes: never wait on its face
+        const bool cvalid = G.jlo + b * TY + cons_j <= G.jhi && G.klo + c * TZ + cons_k <= G.khi;
+        if (!cvalid) in = nullptr;
+        // prefetch ring: ring[u] holds the value consumed at step s0 + u + 1
+        double ring[U];
+        auto fetch = [&](int s, int u) {
+            const int sp = s + D;
+            ring[u] = (in && sp < nsteps) ? ld_relaxed(in + (int64_t)sp * W) : nz0;
+        };
+#pragma unroll
+        for (int u = 0; u < U; u++) fetch(u + 1, u);
+        if (in) {  // value consumed at step 0 lands in slot 1 (= prv of step 0)
+            const double v = D < nsteps ? poll_ready(in + (int64_t)D * W) : nz0;
+            sval[1][in_row][in_col] = v;
+        }
+        for (int s0 = 0; s0 < nsteps; s0 += U) {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int s = s0 + u;
+                if (s >= nsteps) break;
+                __syncthreads();
+                const int cur = s & 1, prv = cur ^ 1;
+                if (active && s > 0) publish(out + (int64_t)(s - 1) * W, sval[prv][out_row][out_col]);
+                if (in) {
+                    double v = ring[u];
+                    if (is_pending(v)) {
+                        v = poll_ready(in + (int64_t)(s + 1 + D) * W);
+                        if (A.trace && !REV) atomicAdd(&A.trace[4 * tile + 2], 1ULL);
+                    }
+                    sval[cur][in_row][in_col] = v;
+                    fetch(s + 1 + U, u);
+                }
+            }
+        }
+        // final publish of the last step's output
+        __syncthreads();
+        if (active) publish(out + (int64_t)(nsteps - 1) * W, sval[(nsteps - 1) & 1][out_row][out_col]);
+        return;
+    }
+
+    // ------------------------------- compute warps ---------------------------
+    const int jj = t % TY, kk = t / TY;
+    const int64_t base = (int64_t)tile * nsteps * TP + t;
+    double *dstL = A.dst + base;
+    const bool valid = G.jlo + b * TY + jj <= G.jhi && G.klo + c * TZ + kk <= G.khi;
+    const int yr = kk + 1, yc = REV ? jj + 2 : jj, zr = REV ? kk + 2 : kk, zc = jj + 1;
+    double pv = nz0;
+    const double sc = A.scale;
+    auto body_step = [&](int s, double a, double pr) {
+        const int cur = s & 1, prv = cur ^ 1;
+        const double yv = sval[prv][yr][yc], zv = sval[prv][zr][zc];
+        const bool row = valid && present(a);
+        double o;
+        if (!REV) {  // _core.pyx:322-332 (absent terms are -0.0: exact no-ops)
+            double tt = ((a + pv) + yv) + zv;
+            double q = tt * pr;
+            if (row) dstL[(int64_t)lstep(s) * TP] = q;
+            o = (sc * pr) * q;
+        } else {     // _core.pyx:333-346
+            double sp = sc * pr;
+            double tt = ((a + sp * pv) + sp * yv) + sp * zv;
+            o = tt * pr;
+            if (row) dstL[(int64_t)lstep(s) * TP] = o;
+        }
+        o = row ? o : nz0;
+        sval[cur][kk + 1][jj + 1] = o;
+        pv = o;
+    };
+    if constexpr (KC == 0) {
+        const double *srcL = A.src + base;
+        const double *preL = A.precon + base;
+        double av[U], bv[U];
+        auto load = [&](int s, int u) {
+            int sl = max(min(lstep(s), nsteps - 1), 0);
+            av[u] = srcL[(int64_t)sl * TP];
+            bv[u] = preL[(int64_t)sl * TP];
+        };
+#pragma unroll
+        for (int u = 0; u < U; u++) load(u, u);
+        for (int s0 = 0; s0 < nsteps; s0 += U) {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int s = s0 + u;
+                if (s >= nsteps) break;
+                __syncthreads();
+                body_step(s, av[u], bv[u]);
+                load(s + U, u);
+            }
+        }
+    } else {
+        // operands arrive KC steps at a time through the bulk-copy engine into
+        // a LANE_NB-deep smem ring (opb[buf][src|precon][KC][TP]), so the only
+        // loads in this SM's LSU queue are the helper's halo polls
+        extern __shared__ __align__(128) double opb[];
+        __shared__ __align__(8) unsigned long long mbar[LANE_NB];
+        const int nch = (nsteps + KC - 1) / KC;
+        const int64_t tbase = (int64_t)tile * nsteps * TP;
+        auto issue = [&](int ch) {  // thread 0 only
+            if (ch >= nch) return;
+            const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
+            const int lo = REV ? nsteps - s0 - cnt : s0;
+            const int buf = ch % LANE_NB;
+            const unsigned bytes = (unsigned)(cnt * TP * 8);
+            mbar_expect_tx(&mbar[buf], 2 * bytes);
+            bulk_g2s(opb + (buf * 2 + 0) * KC * TP, A.src + tbase + (int64_t)lo * TP, bytes,
+                     &mbar[buf]);
+            bulk_g2s(opb + (buf * 2 + 1) * KC * TP, A.precon + tbase + (int64_t)lo * TP, bytes,
+                     &mbar[buf]);
+        };
+        if (t == 0) {
+            for (int q = 0; q < LANE_NB; q++) mbar_init(&mbar[q], 1);
+            mbar_fence_init();
+            for (int q = 0; q < LANE_NB; q++) issue(q);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(TP) : "memory");  // mbarrier init visible
+        for (int ch = 0; ch < nch; ch++) {
+            const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
+            const int buf = ch % LANE_NB;
+            mbar_wait(&mbar[buf], (unsigned)(ch / LANE_NB) & 1u);
+            const double *ab = opb + (buf * 2 + 0) * KC * TP + t;
+            const double *pb = opb + (buf * 2 + 1) * KC * TP + t;
+#pragma unroll
+            for (int u = 0; u < KC; u++) {
+                if (u >= cnt) break;
+                const int s = s0 + u;
+                __syncthreads();
+                if (u == 0 && ch > 0 && t == 0) {
+                    // every thread finished chunk ch-1 before this barrier
+                    fence_proxy_async();
+                    issue(ch - 1 + LANE_NB);
+                }
+                if (A.trace && !REV && tile == A.dbg && t == 0 && s < 1000)
+                    A.trace[16384 + s] = (unsigned long long)clock64();
+                const int idx = REV ? cnt - 1 - u : u;
+                body_step(s, ab[idx * TP], pb[idx * TP]);
+                if (A.trace && !REV && tile == A.dbg && t == 0 && s < 1000)
+                    A.trace[17500 + s] = (unsigned long long)clock64();
+            }
+        }
+    }
+    __syncthreads();  // matches the helper's final barrier
+    if (A.trace && !REV && t == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        A.trace[4 * tile + 0] = t_start;
+        A.trace[4 * tile + 1] = g;
+        A.trace[4 * tile + 3] = (unsigned long long)(b * 65536 + c);
+    }
+}
+
+// L-layout maps: lrow[e] = row at entry e (or -1); posL[row] = e.
+__global__ void k_lane_map(WaveGeom G, Dims d, int TY, int TZ, const uint8_t *__restrict__ isrow,
+                           const int *__restrict__ rowscan, int *__restrict__ lrow,
+                           int *__restrict__ posL, double *__restrict__ absent1,
+                           double *__restrict__ absent2, int64_t nL) {
+    const int TP = TY * TZ;
+    const double ab = __longlong_as_double((long long)WAVE_ABSENT);
+    for (int64_t e = gtid(); e < nL; e += gstride()) {
+        int p = (int)(e % TP);
+        int64_t ts = e / TP;
+        int s = (int)(ts % G.nsteps);
+        int tile = (int)(ts / G.nsteps);
+        int b = tile / G.TC, c = tile % G.TC;
+        int jj = p % TY, kk = p / TY;
+        int i = G.ilo + s - jj - kk, j = G.jlo + b * TY + jj, k = G.klo + c * TZ + kk;
+        int row = -1;
+        if (i >= G.ilo && i <= G.ihi && j <= G.jhi && k <= G.khi) {
+            int64_t cell = i + (int64_t)j * d.nx + (int64_t)k * d.nx * d.ny;
+            if (isrow[cell]) row = rowscan[cell];
+        }
+        lrow[e] = row;
+        if (row >= 0) posL[row] = (int)e;
+        absent1[e] = ab;
+        absent2[e] = ab;
+    }
+}
+
+// vec (compact rows) -> L layout, and back
+__global__ void k_rows_to_lane(const double *__restrict__ v, const int *__restrict__ posL,
+                               int64_t n, double *__restrict__ L, const DevScalars *sc) {
+    if (sc && sc->done) return;
+    for (int64_t r = gtid(); r < n; r += gstride()) L[posL[r]] = v[r];
+}
+__global__ void k_lane_to_rows(const double *__restrict__ L, const int *__restrict__ posL,
+                               int64_t n, double *__restrict__ v, const DevScalars *sc) {
+    if (sc && sc->done) return;
+    for (int64_t r = gtid(); r < n; r += gstride()) v[r] = L[posL[r]];
+}
+
 // halo <- pending marker, ticket <- 0 (skipped after PCG convergence)
 __global__ void k_wave_prep(double *halo, int64_t nh, int *ticket, const DevScalars *sc) {
     if (sc && sc->done) return;
@@ -513,7 +953,9 @@ static TileShape wave_shape() {
 int64_t wave_halo_doubles(int64_t nx, int64_t ny, int64_t nz) {
     TileShape t = wave_shape();
     int64_t tiles = (ny / t.ty + 2) * (nz / t.tz + 2);
-    return tiles * (t.ty + t.tz) * (nx + 2) + 64;
+    // k_wave: [tile][lane][x] (x < nx + 2); k_mic_lane2: [tile][step][lane]
+    // with steps = x span + ty + tz - 2
+    return tiles * (t.ty + t.tz) * (nx + 2 + t.ty + t.tz) + 64;
 }
 
 template <int MODE, int TY, int TZ>
@@ -548,6 +990,96 @@ cudaError_t launch_wave(int mode, const WaveArgs &A, cudaStream_t st) {
         case WV_MIC_BWD: return launch_wave_t<WV_MIC_BWD>(A, st);
         default: return launch_wave_t<WV_GS>(A, st);
     }
+}
+
+int64_t lane_entries(const WaveGeom &g) { return (int64_t)g.TB * g.TC * g.nsteps * g.ty * g.tz; }
+
+int64_t lane_entries_max(int64_t nx, int64_t ny, int64_t nz) {
+    TileShape t = wave_shape();
+    return ((ny + t.ty - 1) / t.ty) * ((nz + t.tz - 1) / t.tz) * (nx + t.ty + t.tz) * t.ty * t.tz;
+}
+
+void launch_lane_map(const WaveGeom &g, const Dims &d, const uint8_t *isrow, const int *rowscan,
+                     int *lrow, int *posL, double *absent1, double *absent2, cudaStream_t st) {
+    int64_t nL = lane_entries(g);
+    k_lane_map<<<nblocks(nL), kThreads, 0, st>>>(g, d, g.ty, g.tz, isrow, rowscan, lrow, posL,
+                                                absent1, absent2, nL);
+}
+
+void launch_rows_to_lane(const double *v, const int *posL, int64_t n, double *L,
+                         const DevScalars *sc, cudaStream_t st) {
+    k_rows_to_lane<<<nblocks(n), kThreads, 0, st>>>(v, posL, n, L, sc);
+}
+
+void launch_lane_to_rows(const double *L, const int *posL, int64_t n, double *v,
+                         const DevScalars *sc, cudaStream_t st) {
+    k_lane_to_rows<<<nblocks(n), kThreads, 0, st>>>(L, posL, n, v, sc);
+}
+
+// prefetch depth (steps) of k_mic_lane2's operand and halo rings
+static int lane_depth() {
+    static const int d = [] {
+        const char *e = getenv("FLIPB200_LANE_DEPTH");
+        return e ? atoi(e) : 4;
+    }();
+    return d;
+}
+// operand staging: 1 = bulk-copy chunks into smem (default), 0 = register ring
+static int lane_chunk() {
+    static const int d = [] {
+        const char *e = getenv("FLIPB200_LANE_BULK");
+        return e ? atoi(e) : 1;
+    }();
+    return d;
+}
+
+template <bool REV, int TY, int TZ>
+static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
+    int64_t tiles = (int64_t)A.geom.TB * A.geom.TC;
+    static const bool v1 = getenv("FLIPB200_LANE_V1") != nullptr;
+    const bool lane2 = TY + TZ <= 32 && !v1;  // step-major halo (k_mic_lane2)
+    int64_t nh = tiles * (TY + TZ) * (lane2 ? A.geom.nsteps : A.geom.ispan_pad);
+    k_wave_prep<<<nblocks(nh), kThreads, 0, st>>>(A.halo_y, nh, A.ticket, A.sc);
+    if constexpr (TY + TZ > 32) {
+        k_mic_lane<REV, TY, TZ><<<(unsigned)tiles, TY * TZ, 0, st>>>(A);
+    } else {
+        if (!lane2) {
+            k_mic_lane<REV, TY, TZ><<<(unsigned)tiles, TY * TZ, 0, st>>>(A);
+            return cudaGetLastError();
+        }
+        LaneArgs B = A;
+        B.halo_z = A.halo_y + tiles * A.geom.nsteps * TZ;
+        if (lane_chunk() > 0) {
+            constexpr int KC = 8;
+            constexpr int smem = LANE_NB * 2 * KC * TY * TZ * 8;
+            static bool attr = [] {
+                cudaFuncSetAttribute(k_mic_lane2<REV, TY, TZ, 4, KC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                return true;
+            }();
+            (void)attr;
+            k_mic_lane2<REV, TY, TZ, 4, KC><<<(unsigned)tiles, TY * TZ + 32, smem, st>>>(B);
+        } else if (lane_depth() == 16)
+            k_mic_lane2<REV, TY, TZ, 16, 0><<<(unsigned)tiles, TY * TZ + 32, 0, st>>>(B);
+        else if (lane_depth() == 8)
+            k_mic_lane2<REV, TY, TZ, 8, 0><<<(unsigned)tiles, TY * TZ + 32, 0, st>>>(B);
+        else
+            k_mic_lane2<REV, TY, TZ, 4, 0><<<(unsigned)tiles, TY * TZ + 32, 0, st>>>(B);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st) {
+    TileShape t = wave_shape();
+#define LANE_CASE(a, b)                                                                   \
+    if (t.ty == a && t.tz == b)                                                           \
+        return rev ? launch_lane_shape<true, a, b>(A, st) : launch_lane_shape<false, a, b>(A, st);
+    LANE_CASE(16, 16)
+    LANE_CASE(32, 8)
+    LANE_CASE(8, 8)
+    LANE_CASE(32, 4)
+#undef LANE_CASE
+    return rev ? launch_lane_shape<true, 16, 8>(A, st) : launch_lane_shape<false, 16, 8>(A, st);
 }
 
 WaveGeom wave_geom(const int lo[3], const int hi[3]) {

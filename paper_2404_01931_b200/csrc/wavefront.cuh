@@ -63,10 +63,30 @@ __device__ __forceinline__ double poll_ready(const double *p) {
     return __longlong_as_double((long long)v);
 }
 
+__device__ __forceinline__ double poll_spin(const double *p) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    } while (v == WAVE_PENDING);
+    return __longlong_as_double((long long)v);
+}
+
 __device__ __forceinline__ double ld_relaxed(const double *p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return __longlong_as_double((long long)v);
+}
+
+// Weak (non-.STRONG) variants for timing experiments: the load never
+// allocates in L1, so every execution still reads the L2 copy.
+__device__ __forceinline__ double ld_na(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.global.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return __longlong_as_double((long long)v);
+}
+
+__device__ __forceinline__ void publish_weak(double *p, double v) {
+    asm volatile("st.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v)) : "memory");
 }
 
 __device__ __forceinline__ void publish(double *p, double v) {
@@ -78,7 +98,31 @@ __device__ __forceinline__ bool is_pending(double v) {
     return (unsigned long long)__double_as_longlong(v) == WAVE_PENDING;
 }
 
+// Lane-major MIC(0) substitution arguments (k_mic_lane).
+struct LaneArgs {
+    WaveGeom geom;
+    const double *src;     // L layout; ABSENT at non-row entries
+    const double *precon;  // L layout
+    double *dst;           // L layout (only row entries written)
+    double *halo_y, *halo_z;
+    double scale;
+    int *ticket;
+    const DevScalars *sc;
+    unsigned long long *trace;  // optional per-step clock of tile 0 lane 0
+    int dbg;                    // ablation bits (timing experiments only)
+    int mode;                   // helper halo policy bits (FLIPB200_LANE_MODE)
+};
+
 cudaError_t launch_wave(int mode, const WaveArgs &A, cudaStream_t st);
+cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st);
+int64_t lane_entries(const WaveGeom &g);
+int64_t lane_entries_max(int64_t nx, int64_t ny, int64_t nz);
+void launch_lane_map(const WaveGeom &g, const Dims &d, const uint8_t *isrow, const int *rowscan,
+                     int *lrow, int *posL, double *absent1, double *absent2, cudaStream_t st);
+void launch_rows_to_lane(const double *v, const int *posL, int64_t n, double *L,
+                         const DevScalars *sc, cudaStream_t st);
+void launch_lane_to_rows(const double *L, const int *posL, int64_t n, double *v,
+                         const DevScalars *sc, cudaStream_t st);
 WaveGeom wave_geom(const int lo[3], const int hi[3]);
 int64_t wave_halo_doubles(int64_t nx, int64_t ny, int64_t nz);
 void launch_cell_flags(const Dims &d, const uint8_t *isrow, unsigned char *cflags,

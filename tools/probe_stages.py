@@ -1,4 +1,6 @@
 import sys, time
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import paper_2404_01931_b200 as P
 res = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 solver = sys.argv[2] if len(sys.argv) > 2 else "pcg"

@@ -1,7 +1,7 @@
 #!/bin/bash
 # quick sweep of wavefront tile shapes / publish periods at 256^3 (2 steps each)
 cd "$(dirname "$0")/.." || exit 1
-for t in 16x8 16x16 32x8 32x16 8x8 32x4; do
+for t in 16x8 16x16 8x8; do
   for p in 2; do
     r=$(FLIPB200_WAVE_TILE=$t FLIPB200_WAVE_PUB=$p timeout 120 python -c "
 import paper_2404_01931_b200 as P

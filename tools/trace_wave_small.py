@@ -1,4 +1,6 @@
 import os, sys
+import os as _os, sys as _sys
+_sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
 import numpy as np
 import paper_2404_01931_b200 as P
 RES = int(os.environ.get("RES", "12"))
