@@ -14,9 +14,10 @@ the reference's own scene builder restated on the device (synthetic, seed 0).
 * e2e       the same metric through the C ABI with HOST buffers: every step
             uploads particles + labels from pinned host memory, steps, and
             downloads the particles.
-* roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_sweep,
-            ~90% of the step): algorithmic bytes (3 x 8 B per row) over the
-            measured per-launch time (CUDA events bracketing each launch).
+* roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_lane2,
+            forward + backward, ~55% of the step): algorithmic bytes (3 x 8 B
+            per row) over the measured per-launch time (CUDA events
+            bracketing each launch on the library's stream).
 * cpu_baseline  the oracle (C restatement of the reference step, all host
             threads) on a bounded sample of the same workload.
 * --impl reference  times the oracle port as the reference arm (the Python
@@ -312,12 +313,12 @@ def run_ours(args):
         alg = pbytes.value / plaunch.value
         achieved = alg / (avg_ms / 1e3) / 1e9
         tr = load_traffic()
-        roof = {"bound": "hbm", "kernel": "k_mic_sweep (MIC(0) substitution wavefront)",
+        roof = {"bound": "hbm", "kernel": "k_mic_lane2 (MIC(0) substitution wavefront, fwd+bwd)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
                 "avg_launch_ms": avg_ms, "launches_timed": int(plaunch.value),
                 "share_of_step": pms.value / ms,
-                "traffic": (tr or {}).get("k_mic_sweep_dram_bytes_per_launch"),
+                "traffic": (tr or {}).get("k_mic_lane2_dram_bytes_per_launch"),
                 "note": "latency-bound dependency wavefront (see DESIGN.md); "
                         "frac is of the HBM copy peak"}
 

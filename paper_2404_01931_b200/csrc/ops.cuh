@@ -36,7 +36,7 @@ struct DevScalars {
 struct Probe {
     int kind = 0;              // 0 off, 1 MIC(0) substitution sweeps
     int used = 0;
-    static constexpr int kMax = 1024;
+    static constexpr int kMax = 4096;
     cudaEvent_t ev[2 * kMax]{};
     double bytes = 0.0;        // algorithmic bytes of the bracketed launches
     int64_t launches = 0;

@@ -735,7 +735,8 @@ __global__ void __launch_bounds__(TY *TZ + 32) k_mic_lane2(LaneArgs A) {
                     double v = ring[u];
                     if (is_pending(v)) {
                         v = poll_ready(in + (int64_t)(s + 1 + D) * W);
-                        if (A.trace && !REV) atomicAdd(&A.trace[4 * tile + 2], 1ULL);
+                        if (A.trace && !REV && tile == A.dbg && s < 1000)
+                            atomicAdd(&A.trace[16384 + 1024 + s], 1ULL);
                     }
                     sval[cur][in_row][in_col] = v;
                     fetch(s + 1 + U, u);
@@ -827,6 +828,7 @@ __global__ void __launch_bounds__(TY *TZ + 32) k_mic_lane2(LaneArgs A) {
             const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
             const int buf = ch % LANE_NB;
             mbar_wait(&mbar[buf], (unsigned)(ch / LANE_NB) & 1u);
+
             const double *ab = opb + (buf * 2 + 0) * KC * TP + t;
             const double *pb = opb + (buf * 2 + 1) * KC * TP + t;
 #pragma unroll
@@ -839,12 +841,15 @@ __global__ void __launch_bounds__(TY *TZ + 32) k_mic_lane2(LaneArgs A) {
                     fence_proxy_async();
                     issue(ch - 1 + LANE_NB);
                 }
-                if (A.trace && !REV && tile == A.dbg && t == 0 && s < 1000)
-                    A.trace[16384 + s] = (unsigned long long)clock64();
+                if (A.trace && !REV && ch == 0 && u == 0 && t == 0) {
+                    // step-0 halo staged: the tile really starts here (LDS orders the stamp)
+                    const double d = sval[1][0][0];
+                    unsigned long long g;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+                    A.trace[4 * tile + 2] = g + (__double_as_longlong(d) == 1 ? 1 : 0);
+                }
                 const int idx = REV ? cnt - 1 - u : u;
                 body_step(s, ab[idx * TP], pb[idx * TP]);
-                if (A.trace && !REV && tile == A.dbg && t == 0 && s < 1000)
-                    A.trace[17500 + s] = (unsigned long long)clock64();
             }
         }
     }
@@ -1055,10 +1060,19 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
             static bool attr = [] {
                 cudaFuncSetAttribute(k_mic_lane2<REV, TY, TZ, 4, KC>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                cudaFuncSetAttribute(k_mic_lane2<REV, TY, TZ, 8, KC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                cudaFuncSetAttribute(k_mic_lane2<REV, TY, TZ, 16, KC>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
                 return true;
             }();
             (void)attr;
-            k_mic_lane2<REV, TY, TZ, 4, KC><<<(unsigned)tiles, TY * TZ + 32, smem, st>>>(B);
+            if (lane_depth() == 16)
+                k_mic_lane2<REV, TY, TZ, 16, KC><<<(unsigned)tiles, TY * TZ + 32, smem, st>>>(B);
+            else if (lane_depth() == 8)
+                k_mic_lane2<REV, TY, TZ, 8, KC><<<(unsigned)tiles, TY * TZ + 32, smem, st>>>(B);
+            else
+                k_mic_lane2<REV, TY, TZ, 4, KC><<<(unsigned)tiles, TY * TZ + 32, smem, st>>>(B);
         } else if (lane_depth() == 16)
             k_mic_lane2<REV, TY, TZ, 16, 0><<<(unsigned)tiles, TY * TZ + 32, 0, st>>>(B);
         else if (lane_depth() == 8)

@@ -10,7 +10,7 @@ enum WaveMode { WV_MIC_BUILD = 0, WV_MIC_FWD = 1, WV_MIC_BWD = 2, WV_GS = 3 };
 #define WAVE_TY 16
 #endif
 #ifndef WAVE_TZ
-#define WAVE_TZ 8
+#define WAVE_TZ 16
 #endif
 
 // "Not yet written" marker pre-filled into the halo buffers.  A NaN with a
