@@ -92,14 +92,12 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
                         t0 = __ldg(offset + cell);
                         t1 = t0 + __ldg(count + cell);
                     }
-                    for (int t = t0; t < t1; t++) {
-                        double hx = hat(div_dtau(d, __ldg(px + t) - fpx));
-                        if (hx == 0.0) continue;  // w = 0 regardless of hy, hz
-                        double hy = hat(div_dtau(d, __ldg(py + t) - fpy));
-                        double hz = hat(div_dtau(d, __ldg(pz + t) - fpz));
-                        double wgt = (hx * hy) * hz;
+                    // two particles per trip with all eight loads issued up
+                    // front (the loop is load-latency bound); the Kahan
+                    // updates still run in particle order
+                    auto kahan = [&](double wgt, double v) {
                         if (wgt > 0.0) {
-                            double yk = wgt * __ldg(vel + t) - cn;
+                            double yk = wgt * v - cn;
                             double tk = num + yk;
                             cn = (tk - num) - yk;
                             num = tk;
@@ -108,7 +106,24 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
                             cd = (tk - dsum) - yk;
                             dsum = tk;
                         }
+                    };
+                    auto weight = [&](double x, double y, double z) {
+                        double hx = hat(div_dtau(d, x - fpx));
+                        double hy = hat(div_dtau(d, y - fpy));
+                        double hz = hat(div_dtau(d, z - fpz));
+                        return (hx * hy) * hz;  // 0 whenever one factor is 0
+                    };
+                    int t = t0;
+                    for (; t + 1 < t1; t += 2) {
+                        const double x0 = __ldg(px + t), x1 = __ldg(px + t + 1);
+                        const double y0 = __ldg(py + t), y1 = __ldg(py + t + 1);
+                        const double z0 = __ldg(pz + t), z1 = __ldg(pz + t + 1);
+                        const double v0 = __ldg(vel + t), v1 = __ldg(vel + t + 1);
+                        const double w0 = weight(x0, y0, z0), w1 = weight(x1, y1, z1);
+                        kahan(w0, v0);
+                        kahan(w1, v1);
                     }
+                    if (t < t1) kahan(weight(__ldg(px + t), __ldg(py + t), __ldg(pz + t)), __ldg(vel + t));
                 }
             }
         }

@@ -20,4 +20,5 @@ print("step  (clock64 cycles) body wait")
 for s in range(min(n - 1, 60)):
     print(f"{s:3d} {(a[s]-t0)/1e3:7.2f} {(bdone[s]-t0)/1e3:7.2f} {bdone[s]-a[s]:6d} {a[s+1]-bdone[s]:6d}")
 body = bdone[:n-1] - a[:n-1]; wait = a[1:n] - bdone[:n-1]
-print("median body", np.median(body), "median wait", np.median(wait))
+polls = tr[16384 + 1024:16384 + 2024]
+print("median body", np.median(body), "median wait", np.median(wait), "sync polls", int(polls.sum()), "first steps", polls[:24].tolist())

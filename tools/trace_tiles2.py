@@ -18,8 +18,10 @@ start = (tr[:, 0] - t0) / 1e3; end = (tr[:, 1] - t0) / 1e3; dur = end - start
 print("tiles", len(tr), "sweep span us", end.max())
 TB, TC = b.max() + 1, c.max() + 1
 S = np.full((TB, TC), np.nan); D = np.full((TB, TC), np.nan); Q = np.zeros((TB, TC))
-S[b, c] = start; D[b, c] = dur; Q[b, c] = tr[:, 2]
+S[b, c] = start; D[b, c] = dur; Q[b, c] = (tr[:, 2] - t0) / 1e3
 np.set_printoptions(linewidth=250, precision=0, suppress=True)
 print("start us (rows b, cols c):"); print(S)
-print("duration us:"); print(D)
-print("sync polls (cumulative over FWD launches):"); print(Q)
+print("end us:"); print(D)
+print("real start (step 0) us:"); print(Q)
+R = (end - (tr[:, 2] - t0) / 1e3)
+print("run time us (end - real start):"); RR = np.full((TB, TC), np.nan); RR[b, c] = R; print(RR)
