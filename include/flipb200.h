@@ -168,6 +168,30 @@ int flip_step(flip_ctx *ctx, const flip_step_params *params, flip_step_report *r
 int flip_run_stages(flip_ctx *ctx, const flip_step_params *params, int32_t first,
                     int32_t last, flip_step_report *report);
 
+/* Slab decomposition support (multi-GPU, one ctx per GPU; the exchanges run
+ * in the host layer over NCCL, paper_2404_01931_b200/dist.py).  Device
+ * pointers stay valid until the next stage call (binning and reseed swap the
+ * particle buffers). */
+typedef struct {
+    double *pos[3], *vel[3];   /* particle SoA, `capacity` entries */
+    int32_t *count, *offset;   /* hash: count[ncells], offset[ncells + 1] */
+    uint8_t *label;            /* ncells */
+    double *u, *v, *w, *p;     /* grid */
+    double *uo, *vo, *wo;      /* grid_old */
+    uint8_t *ku, *kv, *kw;     /* P2G known masks */
+    int64_t capacity, n;
+} flip_dev_ptrs;
+int flip_get_dev_ptrs(flip_ctx *ctx, flip_dev_ptrs *out);
+/* The particle arrays were rewritten in place (device) with n particles, in
+ * any order: the next FLIP_STAGE_BIN recomputes the keys. */
+int flip_set_particle_count(flip_ctx *ctx, int64_t n);
+/* Reseed (particles.py:157-211) only refills/culls cells in z-planes
+ * [k0, k1) (the rank's slab); default the whole grid. */
+int flip_set_slab(flip_ctx *ctx, int64_t k0, int64_t k1);
+/* cell_index_many (binning.py:37-42) of the current particles into a device
+ * int32 buffer of n entries. */
+int flip_particle_cells(flip_ctx *ctx, int32_t *cells_dev);
+
 /* Diagnostics: divergence_field (grid.py:147-156) of the current grid into
  * host div[ncells]; total_energy sums (sim.py:303-315) with numpy pairwise
  * order: ke2 = sum(vx^2+vy^2+vz^2), pe = sum(py - floor_y). */

@@ -79,6 +79,22 @@ class Region(C.Structure):
     ]
 
 
+class DevPtrs(C.Structure):
+    """flip_dev_ptrs: device pointers of a ctx's state (slab decomposition)."""
+    _fields_ = [
+        ("pos", C.c_void_p * 3),
+        ("vel", C.c_void_p * 3),
+        ("count", C.c_void_p),
+        ("offset", C.c_void_p),
+        ("label", C.c_void_p),
+        ("u", C.c_void_p), ("v", C.c_void_p), ("w", C.c_void_p), ("p", C.c_void_p),
+        ("uo", C.c_void_p), ("vo", C.c_void_p), ("wo", C.c_void_p),
+        ("ku", C.c_void_p), ("kv", C.c_void_p), ("kw", C.c_void_p),
+        ("capacity", C.c_int64),
+        ("n", C.c_int64),
+    ]
+
+
 _d = C.POINTER(C.c_double)
 _i64 = C.POINTER(C.c_int64)
 _u8 = C.POINTER(C.c_uint8)
@@ -118,6 +134,10 @@ _SIGNATURES = {
     "flip_set_probe": (C.c_int, [_vp, C.c_int32]),
     "flip_get_probe": (C.c_int, [_vp, _d, _i64, _d]),
     "flip_energy_sums": (C.c_int, [_vp, C.c_double, _d, _d]),
+    "flip_get_dev_ptrs": (C.c_int, [_vp, C.POINTER(DevPtrs)]),
+    "flip_set_particle_count": (C.c_int, [_vp, C.c_int64]),
+    "flip_set_slab": (C.c_int, [_vp, C.c_int64, C.c_int64]),
+    "flip_particle_cells": (C.c_int, [_vp, _vp]),
     "flip_k_sample_velocity_many": (C.c_int, [_d, _d, _d, C.c_int64, C.c_int64, C.c_int64,
                                               C.c_double, C.c_double, C.c_double, C.c_double,
                                               C.c_int64, _d, _d, _d, _d, _d, _d]),

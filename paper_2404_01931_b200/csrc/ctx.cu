@@ -327,6 +327,57 @@ extern "C" int flip_get_particles(flip_ctx *c, double *px, double *py, double *p
     return flip_synchronize(c);
 }
 
+extern "C" int flip_get_dev_ptrs(flip_ctx *c, flip_dev_ptrs *o) {
+    for (int a = 0; a < 3; a++) {
+        o->pos[a] = c->P.a[a];
+        o->vel[a] = c->P.a[3 + a];
+    }
+    o->count = c->count;
+    o->offset = c->offset;
+    o->label = c->label;
+    o->u = c->u;
+    o->v = c->v;
+    o->w = c->w;
+    o->p = c->p;
+    o->uo = c->uo;
+    o->vo = c->vo;
+    o->wo = c->wo;
+    o->ku = c->ku;
+    o->kv = c->kv;
+    o->kw = c->kw;
+    o->capacity = c->cap;
+    o->n = c->n;
+    return 0;
+}
+
+extern "C" int flip_set_particle_count(flip_ctx *c, int64_t n) {
+    if (n < 0 || n > c->cap) {
+        set_error("particle count exceeds capacity");
+        return FLIP_E_CAPACITY;
+    }
+    c->n = n;
+    c->keys_valid = 0;
+    return 0;
+}
+
+extern "C" int flip_set_slab(flip_ctx *c, int64_t k0, int64_t k1) {
+    if (k0 < 0 || k1 > c->d.nz || k0 > k1) {
+        set_error("slab planes out of range");
+        return FLIP_E_ARG;
+    }
+    const int64_t plane = (int64_t)c->d.nx * c->d.ny;
+    c->slab_c0 = k0 * plane;
+    c->slab_c1 = k1 * plane;
+    return 0;
+}
+
+extern "C" int flip_particle_cells(flip_ctx *c, int32_t *cells_dev) {
+    cudaSetDevice(c->device);
+    launch_particle_cells(*c, cells_dev);
+    FLIP_CUDA_OK(cudaGetLastError());
+    return 0;
+}
+
 extern "C" int flip_particle_count(flip_ctx *c, int64_t *n) {
     *n = c->n;
     return 0;

@@ -49,6 +49,7 @@ struct Ctx {
     int64_t ncells = 0, nfu = 0, nfv = 0, nfw = 0;
     int64_t cap = 0;        // particle capacity
     int64_t n = 0;          // particle count (host mirror)
+    int64_t slab_c0 = 0, slab_c1 = -1;  // reseed cell range (flip_set_slab); -1: all
     ParticlePtrs P{}, Q{};  // current and back particle buffers
     double *u = nullptr, *v = nullptr, *w = nullptr, *p = nullptr;
     uint8_t *label = nullptr;
@@ -113,6 +114,7 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep);  
 void stage_apply_gradient(Ctx &c, const flip_step_params &prm);
 void stage_g2p(Ctx &c, const flip_step_params &prm);
 void stage_reseed(Ctx &c, const flip_step_params &prm);
+void launch_particle_cells(Ctx &c, int *out);
 
 void launch_set_solid_shell(Ctx &c);
 int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed);

@@ -209,18 +209,31 @@ void launch_sample_many(const Dims &d, const double *u, const double *v, const d
     k_sample_many<<<nblocks(n), kThreads, 0, st>>>(d, u, v, w, n, px, py, pz, vx, vy, vz);
 }
 
+// cell_index_many of the current particles (flip_particle_cells)
+__global__ void k_particle_cells(ParticlePtrs P, int64_t n, Dims d, int *__restrict__ out) {
+    for (int64_t t = gtid(); t < n; t += gstride()) out[t] = cell_of(d, P.a[0][t], P.a[1][t], P.a[2][t]);
+}
+
+void launch_particle_cells(Ctx &c, int *out) {
+    if (c.n <= 0) return;
+    k_particle_cells<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.d, out);
+    c.launches++;
+}
+
 // ---------------------------------------------------------------- reseed --
 // flipsim/particles.py:157-178: per-cell refill/cull counts.
+// Cells outside [c0, c1) (another rank's slab) are left alone.
 __global__ void k_reseed_count(const int *__restrict__ count, const uint8_t *__restrict__ label,
                                int64_t nc, int density, int *__restrict__ nadd,
-                               int *__restrict__ new_count, DevScalars *sc) {
+                               int *__restrict__ new_count, DevScalars *sc, int64_t c0, int64_t c1) {
     int target = density * density * density;
     if (target > MAX_PER_CELL) target = MAX_PER_CELL;
     int changed = 0;
     for (int64_t c = gtid(); c < nc; c += gstride()) {
         int cnt = count[c];
         int add = 0;
-        if (label[c] == FLUID && cnt < MIN_PER_CELL) add = target - cnt > 0 ? target - cnt : 0;
+        if (label[c] == FLUID && cnt < MIN_PER_CELL && c >= c0 && c < c1)
+            add = target - cnt > 0 ? target - cnt : 0;
         nadd[c] = add;
         new_count[c] = (cnt < MAX_PER_CELL ? cnt : MAX_PER_CELL) + add;
         changed |= (add > 0) | (cnt > MAX_PER_CELL);
@@ -288,8 +301,10 @@ void stage_reseed(Ctx &c, const flip_step_params &prm) {
         c.launches++;
     }
     cudaMemsetAsync(&c.sc->reseed_changed, 0, sizeof(int), c.st);
+    const int64_t c1 = c.slab_c1 < 0 ? c.ncells : c.slab_c1;
     k_reseed_count<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.count, c.label, c.ncells,
-                                                             prm.density, nadd, new_count, c.sc);
+                                                             prm.density, nadd, new_count, c.sc,
+                                                             c.slab_c0, c1);
     exclusive_scan(ArrayIn{new_count}, c.ncells, new_offset, new_offset + c.ncells, c.scan_tmp,
                    c.st);
     c.launches += 4;

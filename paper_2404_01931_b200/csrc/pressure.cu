@@ -217,41 +217,67 @@ __device__ __forceinline__ int64_t pw_split(int64_t n) {
     return n2 - n2 % 8;
 }
 
+// Element loaders for the pairwise dot: ld(i) returns the i-th summand and
+// is called exactly once per element, so a loader may also produce a vector
+// (the fused matvec and lane-gather variants below).
+struct LdProd {
+    const double *a, *b;
+    __device__ __forceinline__ double operator()(int64_t i) const { return b ? a[i] * b[i] : a[i]; }
+};
+
 // 8 lanes (aligned group) evaluate one leaf; result valid in group lane 0.
-__device__ double pw_leaf8(const double *__restrict__ a, const double *__restrict__ b, int64_t s,
-                           int64_t len, int g) {
+template <class LD>
+__device__ __forceinline__ double pw_leaf8(const LD &ld, int64_t s, int64_t len, int g) {
     unsigned mask = 0xffu << (threadIdx.x & 24);
     double res = 0.0;
     if (len < 8) {
         if (g == 0)
-            for (int64_t i = 0; i < len; i++) res += b ? a[s + i] * b[s + i] : a[s + i];
+            for (int64_t i = 0; i < len; i++) res += ld(s + i);
         return res;
     }
-    int64_t m = len - len % 8;
-    double r = b ? a[s + g] * b[s + g] : a[s + g];
-    for (int64_t i = 8; i < m; i += 8) r += b ? a[s + i + g] * b[s + i + g] : a[s + i + g];
+    // len <= 128: a lane owns at most 16 summands; load them all first (the
+    // loads are independent), then accumulate in numpy's order
+    const int cntv = (int)(len / 8);
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) v[k] = k < cntv ? ld(s + g + 8 * k) : 0.0;
+    double r = v[0];
+#pragma unroll
+    for (int k = 1; k < 16; k++)
+        if (k < cntv) r += v[k];
+    const int64_t m = (int64_t)cntv * 8;
     r = r + __shfl_xor_sync(mask, r, 1, 8);
     r = r + __shfl_xor_sync(mask, r, 2, 8);
     r = r + __shfl_xor_sync(mask, r, 4, 8);
     if (g == 0)
-        for (int64_t i = m; i < len; i++) r += b ? a[s + i] * b[s + i] : a[s + i];
+        for (int64_t i = m; i < len; i++) r += ld(s + i);
     return r;
 }
 
-// Exact recursive evaluation of a (small) subtree by one 8-lane group.
-__device__ double pw_node8(const double *__restrict__ a, const double *__restrict__ b, int64_t s,
-                           int64_t len, int g, int depth) {
-    if (len <= 128) return pw_leaf8(a, b, s, len, g);
-    int64_t n2 = pw_split(len);
-    double l = pw_node8(a, b, s, n2, g, depth + 1);
-    double r = pw_node8(a, b, s + n2, len - n2, g, depth + 1);
-    return l + r;
+// Exact evaluation of a (small) subtree by one 8-lane group.  Nodes at the
+// cut level differ in length by a few multiples of 8 and one of them is
+// <= 128, so two more splits always reach the leaves; the depth is a
+// template parameter so everything inlines (no call stack).
+template <int DEPTH, class LD>
+__device__ __forceinline__ double pw_node8(const LD &ld, int64_t s, int64_t len, int g) {
+    if constexpr (DEPTH == 0) {
+        return pw_leaf8(ld, s, len, g);
+    } else {
+        if (len <= 128) return pw_leaf8(ld, s, len, g);
+        int64_t n2 = pw_split(len);
+        double l = pw_node8<DEPTH - 1>(ld, s, n2, g);
+        double r = pw_node8<DEPTH - 1>(ld, s + n2, len - n2, g);
+        return l + r;
+    }
 }
 
 // Phase 1: the 2^cut nodes at the deepest complete level, 32 per block, then
 // a perfect-tree reduction of the block's 32 node sums (pairs 2i, 2i+1 first).
-__global__ void k_dot_nodes(const double *__restrict__ a, const double *__restrict__ b, int64_t n,
-                            int cut, double *__restrict__ out) {
+// Skipped once sc->done (the epilogue then ignores the sum).
+template <class LD>
+__global__ void k_dot_nodes(LD ld, int64_t n, int cut, double *__restrict__ out,
+                            const DevScalars *sc) {
+    if (sc && sc->done) return;
     __shared__ double sv[32];
     int64_t nodes = (int64_t)1 << cut;
     int64_t node = (int64_t)blockIdx.x * 32 + (threadIdx.x >> 3);
@@ -268,7 +294,7 @@ __global__ void k_dot_nodes(const double *__restrict__ a, const double *__restri
                 len = n2;
             }
         }
-        val = pw_node8(a, b, s, len, g, 0);
+        val = pw_node8<2>(ld, s, len, g);
     }
     if (g == 0) sv[threadIdx.x >> 3] = val;
     __syncthreads();
@@ -352,13 +378,16 @@ int64_t dot_tmp_doubles(int64_t n) {
 }
 
 // epi/sc select a fused scalar update; for EPI_STORE the sum goes to *out_dev.
-void launch_dot(const double *a, const double *b, int64_t n, double *tmp, double *out_dev, int epi,
-                DevScalars *sc, cudaStream_t st, int64_t *launches) {
+template <class LD>
+static void launch_dot_f(const LD &ld, int64_t n, double *tmp, double *out_dev, int epi,
+                         DevScalars *sc, cudaStream_t st, int64_t *launches) {
     int cut = pw_cut(n > 0 ? n : 1);
     int64_t nodes = (int64_t)1 << cut;
     int64_t nb1 = (nodes + 31) / 32;
     double *p0 = tmp, *p1 = tmp + nb1;
-    k_dot_nodes<<<(unsigned)nb1, 256, 0, st>>>(a, b, n, cut, p0);
+    // only the solver's in-loop dots may skip their work after convergence
+    const bool skip = epi == EPI_CURV || epi == EPI_SIGMA_NEW;
+    k_dot_nodes<LD><<<(unsigned)nb1, 256, 0, st>>>(ld, n, cut, p0, skip ? sc : nullptr);
     (*launches)++;
     int64_t cnt = nb1;
     double *in = p0, *outp = p1;
@@ -370,6 +399,11 @@ void launch_dot(const double *a, const double *b, int64_t n, double *tmp, double
         cnt = blocks;
         std::swap(in, outp);
     }
+}
+
+void launch_dot(const double *a, const double *b, int64_t n, double *tmp, double *out_dev, int epi,
+                DevScalars *sc, cudaStream_t st, int64_t *launches) {
+    launch_dot_f(LdProd{a, b}, n, tmp, out_dev, epi, sc, st, launches);
 }
 
 void launch_pairwise_dot(const double *a, const double *b, int64_t n, double *tmp, double *out_dev,
@@ -419,6 +453,35 @@ __global__ void k_matvec(SysView S, const double *__restrict__ x, double *__rest
         if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(resmax, m);
     }
 }
+
+// q = A s fused into the s.q dot (pressure.py:315-316): k_matvec's
+// arithmetic for row r, q[r] written, s[r]*q[r] returned.
+struct LdMatvecDot {
+    SysView S;
+    const double *x;
+    double *y;
+    __device__ __forceinline__ double operator()(int64_t r) const {
+        double s = nbr_sum(S.nbr, S.ldn, r, x);
+        double xr = x[r];
+        double yr = S.scale * (S.diag[r] * xr - s);
+        y[r] = yr;
+        return xr * yr;
+    }
+};
+
+// z taken from the lane-major layout of the MIC(0) sweep (k_lane_to_rows
+// fused into the z.r dot): z[r] written, z[r]*r[r] returned.
+struct LdLaneDot {
+    const double *zL;
+    const int *posL;
+    double *z;
+    const double *r;
+    __device__ __forceinline__ double operator()(int64_t i) const {
+        double zi = zL[posL[i]];
+        z[i] = zi;
+        return zi * r[i];
+    }
+};
 
 // _core.pyx:216-234 (out of place)
 __global__ void k_jacobi(SysView S, const double *__restrict__ x, double *__restrict__ out,
@@ -677,9 +740,11 @@ __global__ void k_check_diag_final(SysView S, DevScalars *sc, const unsigned lon
 }
 
 // x += alpha s; r -= alpha q; res = max|r|  (pressure.py:321-323)
+// (rL, posL): also scatter r into the MIC(0) sweep's lane layout
+// (k_rows_to_lane fused).
 __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
                              const double *__restrict__ s, const double *__restrict__ q,
-                             DevScalars *sc) {
+                             DevScalars *sc, double *__restrict__ rL, const int *__restrict__ posL) {
     if (sc->done) return;
     double alpha = sc->alpha;
     double m = 0.0;
@@ -687,6 +752,7 @@ __global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restri
         x[i] = x[i] + alpha * s[i];
         double ri = r[i] - alpha * q[i];
         r[i] = ri;
+        if (rL) rL[posL[i]] = ri;
         m = fmax(m, fabs(ri));
     }
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -821,13 +887,15 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
 }
 
 // z = M^-1 r for the selected preconditioner (pressure.py:284-300).
+// fused: the lane path's r -> L and L -> z conversions are done by the
+// caller's k_pcg_update and z.r dot (r already in Lb.rL, z left in Lb.zL).
 static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                      const SweepLevels &LV, const double *r, double *z, DevScalars *sc,
-                     cudaStream_t st, int64_t *launches) {
+                     cudaStream_t st, int64_t *launches, bool fused = false) {
     if (cfg.precond == FLIP_PRECOND_MIC0 && LV.lane) {
         // r -> L layout, forward (L), backward (L), back to rows
         const LaneBufs &Lb = *LV.lane;
-        launch_rows_to_lane(r, Lb.posL, S.n, Lb.rL, sc, st);
+        if (!fused) launch_rows_to_lane(r, Lb.posL, S.n, Lb.rL, sc, st);
         Probe *pb = LV.probe;
         for (int rev = 0; rev < 2; rev++) {
             LaneArgs A = Lb.args;
@@ -846,8 +914,8 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 pb->bytes += 24.0 * (double)S.n;  // src + precon read, dst written per row
             }
         }
-        launch_lane_to_rows(Lb.zL, Lb.posL, S.n, z, sc, st);
-        *launches += 2 * 2 + 2;
+        if (!fused) launch_lane_to_rows(Lb.zL, Lb.posL, S.n, z, sc, st);
+        *launches += 2 * 2 + (fused ? 0 : 2);
     } else if (cfg.precond == FLIP_PRECOND_MIC0) {
         // forward substitution into tq, then backward into z
         do_sweep<SW_MIC_FWD>(S, LV, r, B.tq, B.precon, sc, st, launches);
@@ -900,14 +968,33 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
         int64_t batch = std::min<int64_t>(every, cfg.max_iters - it);
         for (int64_t b = 0; b < batch; b++) {
             if (!relax) {  // pressure.py:314-331
-                k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr, nullptr, sc, 1);
-                launch_dot(B.s, B.q, n, B.dot_tmp, nullptr, EPI_CURV, sc, st, launches);
-                k_pcg_update<<<nblocks(n), kThreads, 0, st>>>(n, B.x, B.r, B.s, B.q, sc);
+                // r also lands in the lane layout and z comes back through the
+                // z.r dot (pressure.py:314-331); q = A s can be fused into the
+                // s.q dot too (FLIPB200_FUSE_MATVEC, slower: 8-lane groups
+                // coalesce the stencil gathers worse than k_matvec)
+                const bool lane = cfg.precond == FLIP_PRECOND_MIC0 && LV.lane;
+                static const bool fuse_mv = getenv("FLIPB200_FUSE_MATVEC") != nullptr;
+                if (fuse_mv) {
+                    launch_dot_f(LdMatvecDot{S, B.s, B.q}, n, B.dot_tmp, nullptr, EPI_CURV, sc,
+                                 st, launches);
+                } else {
+                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
+                                                              nullptr, sc, 1);
+                    launch_dot(B.s, B.q, n, B.dot_tmp, nullptr, EPI_CURV, sc, st, launches);
+                    (*launches)++;
+                }
+                k_pcg_update<<<nblocks(n), kThreads, 0, st>>>(n, B.x, B.r, B.s, B.q, sc,
+                                                              lane ? LV.lane->rL : nullptr,
+                                                              lane ? LV.lane->posL : nullptr);
                 k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
-                apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches);
-                launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA_NEW, sc, st, launches);
+                apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
+                if (lane)
+                    launch_dot_f(LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, n, B.dot_tmp,
+                                 nullptr, EPI_SIGMA_NEW, sc, st, launches);
+                else
+                    launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA_NEW, sc, st, launches);
                 k_pcg_dir<<<nblocks(n), kThreads, 0, st>>>(n, B.s, B.z, sc);
-                *launches += 4;
+                *launches += 3;
             } else {  // pressure.py:209-213
                 if (cfg.solver == FLIP_SOLVER_JACOBI) {
                     k_jacobi<<<nblocks(n), kThreads, 0, st>>>(S, B.x, B.xtmp, sc, 1);
