@@ -24,8 +24,11 @@ the reference's own scene builder restated on the device (synthetic, seed 0).
             reference cannot travel to the GPU box; oracle/ is its bit-exact
             C restatement, pinned by tests/).
 
-Multi-GPU (torchrun, one process per GPU): until the z-slab decomposition
-lands every rank runs an independent replica ("scaling": "weak").
+Multi-GPU (torchrun, one process per GPU, NCCL): the z-slab decomposition of
+paper_2404_01931_b200/dist.py -- particle stages sharded by slab (migration,
+ghost planes, owned-face all-gather, dt/label allreduces), the grid stages
+and the MIC(0)-PCG solve replicated.  The total workload stays the 256^3
+scene ("scaling": "strong"); results are bit-identical to one GPU.
 """
 
 from __future__ import annotations
@@ -188,11 +191,14 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: ranks sharing one GPU over gloo (no NCCL with duplicate GPUs)
+    if os.environ.get("FLIPB200_SAME_GPU"):
+        local = 0
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("FLIPB200_DIST_BACKEND", "nccl"))
     torch.cuda.set_device(local)
 
     import paper_2404_01931_b200 as P
@@ -200,12 +206,18 @@ def run_ours(args):
     from paper_2404_01931_b200._lib import LIB, check
 
     spec = P.SceneSpec(name=args.scene, res=args.res, solver=args.solver)
-    st = P.make_scene(spec, rng_seed=0, device=local)
+    if world > 1:
+        from paper_2404_01931_b200 import dist as D
+        st = D.make_scene(spec, rng_seed=0, device=local)
+        do_step = D.step
+    else:
+        st = P.make_scene(spec, rng_seed=0, device=local)
+        do_step = P.step
     dev = st.device
     n0 = st.particles.count
     warm = max(3, args.warmup)
     for _ in range(warm):
-        P.step(st, spec)
+        do_step(st, spec)
     stream = torch.cuda.ExternalStream(dev.stream_ptr(), device=local)
 
     def barrier():
@@ -227,7 +239,7 @@ def run_ours(args):
     iters = []
     for _ in range(args.steps):
         parts += st.particles.count
-        rep = P.step(st, spec)
+        rep = do_step(st, spec)
         launches += rep.gpu_launches
         iters.append(rep.solver_iterations)
         for k, v in rep.timings.as_dict().items():
@@ -244,11 +256,13 @@ def run_ours(args):
     total_parts = parts
     ms_max = ms
     if dist is not None:
-        t = torch.tensor([ms, float(parts)], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([ms, float(parts), float(launches)], device=f"cuda:{local}",
+                         dtype=torch.float64)
         tm = t.clone()
         dist.all_reduce(tm[0:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
-        ms_max, total_parts = float(tm[0]), float(t[1])
+        dist.all_reduce(t[1:3], op=dist.ReduceOp.SUM)
+        ms_max, total_parts, launches = float(tm[0]), float(t[1]), int(t[2])
+        n0 = int(st.slab.tr.allreduce_sum_int(n0))
     value = total_parts / (ms_max / 1e3)
 
     # ---------------- end to end through the C ABI (host buffers) ----------
@@ -276,12 +290,18 @@ def run_ours(args):
             check(LIB.flip_set_grid(dev.ctx, None, None, None, None,
                                     lab.ctypes.data_as(_lib._u8)))
             h2d += 48 * n + lab.size
-            params.reseed_seed = P.rng.derive_seed(st.rng_seed, st.step_count + 1)
-            rc = LIB.flip_step(dev.ctx, C.byref(params), C.byref(repc))
-            check(rc)
-            st.step_count += 1
-            e2e_parts += n
-            n = int(repc.particle_count)
+            if world > 1:
+                dev.bump()
+                do_step(st, spec)   # the slab step through the public API
+                e2e_parts += n
+                n = dev.count()
+            else:
+                params.reseed_seed = P.rng.derive_seed(st.rng_seed, st.step_count + 1)
+                rc = LIB.flip_step(dev.ctx, C.byref(params), C.byref(repc))
+                check(rc)
+                st.step_count += 1
+                e2e_parts += n
+                n = int(repc.particle_count)
             if n > cap:
                 raise RuntimeError("e2e host buffers too small")
             # result back to pinned host memory
@@ -290,16 +310,21 @@ def run_ours(args):
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         dev.bump()
-        w = torch.tensor([wall, float(e2e_parts)], dtype=torch.float64, device=f"cuda:{local}")
+        w = torch.tensor([wall, float(e2e_parts), float(h2d), float(d2h)], dtype=torch.float64,
+                         device=f"cuda:{local}")
         if dist is not None:
             wm = w.clone()
             dist.all_reduce(wm[0:1], op=dist.ReduceOp.MAX)
-            dist.all_reduce(w[1:2], op=dist.ReduceOp.SUM)
+            dist.all_reduce(w[1:4], op=dist.ReduceOp.SUM)
             w[0] = wm[0]
+            h2d, d2h = int(w[2]), int(w[3])
         e2e = {"value": float(w[1]) / float(w[0]), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d // e2e_steps), "d2h_bytes_per_step": int(d2h // e2e_steps),
                "timing": "wall clock around K synchronous C-ABI steps incl. pinned H2D/D2H"}
 
+    n_final = dev.count()
+    if dist is not None:
+        n_final = int(st.slab.tr.allreduce_sum_int(n_final))
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -318,7 +343,9 @@ def run_ours(args):
                 "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
                 "avg_launch_ms": avg_ms, "launches_timed": int(plaunch.value),
                 "share_of_step": pms.value / ms,
-                "traffic": (tr or {}).get("k_mic_lane2_dram_bytes_per_launch"),
+                # the ncu capture is of the 256^3 dam-break sweep
+                "traffic": ((tr or {}).get("k_mic_lane2_dram_bytes_per_launch")
+                            if (args.res, args.scene) == (256, "dam-break") else None),
                 "note": "latency-bound dependency wavefront (see DESIGN.md); "
                         "frac is of the HBM copy peak"}
 
@@ -336,15 +363,17 @@ def run_ours(args):
 
     line = {"metric": BASE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": warm, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference dam-break scene builder on the device, seed 0)",
             "config": dict(workload(args), particles_initial=n0,
-                           parallelism="replicas" if world > 1 else "single"),
+                           parallelism=(f"slab-z{world}: particle stages sharded, grid stages "
+                                        "and MIC(0)-PCG replicated" if world > 1 else "single")),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu,
             "detail": {"stage_ms_mean": {k: v / args.steps for k, v in stage.items()},
                        "solver_iterations": iters,
-                       "particles_final": st.particles.count}}
+                       "particles_final": n_final}}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
