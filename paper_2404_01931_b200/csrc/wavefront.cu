@@ -293,11 +293,7 @@ __global__ void __launch_bounds__(TY *TZ) k_wave(WaveArgs A) {
 // so a single int load per step carries everything.  Non-rows publish the
 // ABSENT marker (shared memory and halos alike), so a value and its presence
 // travel in one 8-byte word and the step body is branch-light.
-constexpr unsigned long long WAVE_ABSENT = 0x7FF4DEAD5EED0002ULL;
 
-__device__ __forceinline__ bool present(double v) {
-    return (unsigned long long)__double_as_longlong(v) != WAVE_ABSENT;
-}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -594,44 +590,6 @@ __global__ void __launch_bounds__(TY *TZ) k_mic_lane(LaneArgs A) {
 }
 
 // ---------------------------------------------------------------------------
-// ---- bulk-copy (TMA engine, non-tensor) + mbarrier helpers -----------------
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// global -> shared bulk copy, completion counted on *bar (bytes % 16 == 0)
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
-                                         unsigned long long *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
 // k_mic_lane2: warp-specialised lane-major MIC(0) substitution.
 //
 // Warps 0..TP/32-1 compute; one extra helper warp owns every cross-tile
@@ -1092,7 +1050,7 @@ static TileShape wave_shape() {
 
 int64_t wave_halo_doubles(int64_t nx, int64_t ny, int64_t nz) {
     TileShape t = wave_shape();
-    int64_t tiles = (ny / t.ty + 2) * (nz / t.tz + 2);
+    int64_t tiles = (ny / t.ty + 9) * (nz / t.tz + 9);  // + cluster padding
     // k_wave: [tile][lane][x] (x < nx + 2); k_mic_lane2: [tile][step][lane]
     // with steps = x span + ty + tz - 2
     return tiles * (t.ty + t.tz) * (nx + 2 + t.ty + t.tz) + 64;
@@ -1136,7 +1094,9 @@ int64_t lane_entries(const WaveGeom &g) { return (int64_t)g.TB * g.TC * g.nsteps
 
 int64_t lane_entries_max(int64_t nx, int64_t ny, int64_t nz) {
     TileShape t = wave_shape();
-    return ((ny + t.ty - 1) / t.ty) * ((nz + t.tz - 1) / t.tz) * (nx + t.ty + t.tz) * t.ty * t.tz;
+    // + cluster padding (wave_geom): at most 7 tiles per axis
+    return ((ny + t.ty - 1) / t.ty + 7) * ((nz + t.tz - 1) / t.tz + 7) * (nx + t.ty + t.tz) * t.ty *
+           t.tz;
 }
 
 void launch_lane_map(const WaveGeom &g, const Dims &d, const uint8_t *isrow, const int *rowscan,
@@ -1189,6 +1149,10 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
         }
         LaneArgs B = A;
         B.halo_z = A.halo_y + tiles * A.geom.nsteps * TZ;
+        if (TY == 16 && TZ == 16) {
+            cudaError_t e = launch_mic_cluster(REV, B, st);
+            if (e != cudaErrorNotSupported) return e;
+        }
         static const bool v3 = getenv("FLIPB200_LANE_V3") != nullptr;
         if (v3) {
             constexpr int KC = 8;
@@ -1255,6 +1219,12 @@ WaveGeom wave_geom(const int lo[3], const int hi[3]) {
     g.tz = t.tz;
     g.TB = (hi[1] - lo[1] + t.ty) / t.ty;
     g.TC = (hi[2] - lo[2] + t.tz) / t.tz;
+    int cy, cz;
+    if (t.ty == 16 && t.tz == 16 && mic_cluster_pad(&cy, &cz)) {
+        // whole clusters of tiles (the padding tiles hold no rows)
+        g.TB = (g.TB + cy - 1) / cy * cy;
+        g.TC = (g.TC + cz - 1) / cz * cz;
+    }
     g.ispan = hi[0] - lo[0] + 1;
     g.ispan_pad = (g.ispan + 1) & ~1;
     g.nsteps = g.ispan + (t.ty - 1) + (t.tz - 1);

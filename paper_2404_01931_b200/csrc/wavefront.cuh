@@ -18,6 +18,8 @@ enum WaveMode { WV_MIC_BUILD = 0, WV_MIC_FWD = 1, WV_MIC_BWD = 2, WV_GS = 3 };
 // consumer reading one 8-byte word sees either the marker or the final value:
 // the data is its own ready flag and no fences are needed.
 constexpr unsigned long long WAVE_PENDING = 0x7FF4DEAD5EED0001ULL;
+// Entry of the lane-major layout that holds no row (k_lane_map).
+constexpr unsigned long long WAVE_ABSENT = 0x7FF4DEAD5EED0002ULL;
 
 // Per-cell sweep flags (built once per assembly, k_cell_flags).
 constexpr unsigned char CF_ROW = 1;                                      // cell is a row
@@ -94,8 +96,50 @@ __device__ __forceinline__ void publish(double *p, double v) {
                  : "memory");
 }
 
+__device__ __forceinline__ bool present(double v) {
+    return (unsigned long long)__double_as_longlong(v) != WAVE_ABSENT;
+}
+
 __device__ __forceinline__ bool is_pending(double v) {
     return (unsigned long long)__double_as_longlong(v) == WAVE_PENDING;
+}
+
+// ---- bulk-copy (TMA engine, non-tensor) + mbarrier helpers -----------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy, completion counted on *bar (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Lane-major MIC(0) substitution arguments (k_mic_lane).
@@ -115,6 +159,9 @@ struct LaneArgs {
 
 cudaError_t launch_wave(int mode, const WaveArgs &A, cudaStream_t st);
 cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st);
+// wavecl.cu: cluster/DSMEM variant (FLIPB200_CLUSTER=CYxCZ); NotSupported if off
+cudaError_t launch_mic_cluster(bool rev, const LaneArgs &A, cudaStream_t st);
+int mic_cluster_pad(int *cy, int *cz);
 int64_t lane_entries(const WaveGeom &g);
 int64_t lane_entries_max(int64_t nx, int64_t ny, int64_t nz);
 void launch_lane_map(const WaveGeom &g, const Dims &d, const uint8_t *isrow, const int *rowscan,
