@@ -887,6 +887,10 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
 }
 
 // z = M^-1 r for the selected preconditioner (pressure.py:284-300).
+// First sweep-launch failure of the current solve (configuration errors
+// such as a shared-memory request are not sticky CUDA errors).
+static cudaError_t g_sweep_launch_err = cudaSuccess;
+
 // fused: the lane path's r -> L and L -> z conversions are done by the
 // caller's k_pcg_update and z.r dot (r already in Lb.rL, z left in Lb.zL).
 static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
@@ -906,7 +910,10 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             bool probed = pb && pb->kind == 1 && pb->used < Probe::kMax;
             if (probed) cudaEventRecord(pb->ev[2 * pb->used], st);
             cudaError_t e = launch_mic_lane(rev != 0, A, st);
-            if (e != cudaSuccess) set_error(std::string("lane sweep launch: ") + cudaGetErrorString(e));
+            if (e != cudaSuccess) {
+                set_error(std::string("lane sweep launch: ") + cudaGetErrorString(e));
+                g_sweep_launch_err = e;  // fails the solve (stage_project)
+            }
             if (probed) {
                 cudaEventRecord(pb->ev[2 * pb->used + 1], st);
                 pb->used++;
@@ -1134,8 +1141,13 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     SolveBufs B{c.x, c.r, c.z, c.s, c.q, c.tq, c.precon, c.xtmp, c.dot_part, c.scan_tmp,
                 c.u64_scratch};
     SolveOut o{};
+    g_sweep_launch_err = cudaSuccess;
     int rc = run_solve(S, cfg, B, LV, c.sc, c.sch, st, &c.launches, &o);
     if (rc) return rc;
+    if (g_sweep_launch_err != cudaSuccess) {
+        set_error(std::string("MIC(0) sweep launch failed: ") + cudaGetErrorString(g_sweep_launch_err));
+        return FLIP_E_CUDA;
+    }
     rep->solver_iterations = o.iterations;
     rep->solver_residual = o.residual;
     rep->solver_converged = o.converged;

@@ -296,12 +296,16 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
 static int cluster_shape(int *cy, int *cz) {
     static int y = -1, z = -1;
     if (y < 0) {
-        y = z = 0;
+        // default 4 x 4 tiles per cluster (fastest measured at 256^3);
+        // FLIPB200_CLUSTER=CYxCZ picks another shape, =off disables
+        y = z = 4;
         if (const char *e = getenv("FLIPB200_CLUSTER")) {
             int a = 0, b = 0;
             if (sscanf(e, "%dx%d", &a, &b) == 2) {
                 y = a;
                 z = b;
+            } else {
+                y = z = 0;
             }
         }
     }
@@ -340,7 +344,8 @@ static cudaError_t launch_cl(const LaneArgs &A, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_mic_cl<REV, CY, CZ>, A);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_cl<REV, CY, CZ>, A);
+    return e != cudaSuccess ? e : cudaPeekAtLastError();
 }
 
 // Returns cudaErrorNotSupported when no cluster shape is configured (the

@@ -1032,7 +1032,7 @@ void launch_cell_flags(const Dims &d, const uint8_t *isrow, unsigned char *cflag
 struct TileShape {
     int ty, tz;
 };
-static const TileShape kShapes[] = {{16, 8}, {16, 16}, {32, 8}, {8, 8}, {32, 4}};
+static const TileShape kShapes[] = {{16, 8}, {16, 16}, {32, 8}, {8, 8}, {32, 4}, {32, 16}};
 
 static TileShape wave_shape() {
     static TileShape sh = [] {
@@ -1137,7 +1137,7 @@ template <bool REV, int TY, int TZ>
 static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
     int64_t tiles = (int64_t)A.geom.TB * A.geom.TC;
     static const bool v1 = getenv("FLIPB200_LANE_V1") != nullptr;
-    const bool lane2 = TY + TZ <= 32 && !v1;  // step-major halo (k_mic_lane2)
+    const bool lane2 = TY + TZ <= 32 && !v1;  // step-major halo (k_mic_lane2 / k_mic_cl)
     int64_t nh = tiles * (TY + TZ) * (lane2 ? (int64_t)A.geom.nsteps : A.geom.ispan_pad);
     k_wave_prep<<<nblocks(nh), kThreads, 0, st>>>(A.halo_y, nh, A.ticket, A.sc);
     if constexpr (TY + TZ > 32) {
@@ -1145,7 +1145,7 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
     } else {
         if (!lane2) {
             k_mic_lane<REV, TY, TZ><<<(unsigned)tiles, TY * TZ, 0, st>>>(A);
-            return cudaGetLastError();
+            return cudaPeekAtLastError();
         }
         LaneArgs B = A;
         B.halo_z = A.halo_y + tiles * A.geom.nsteps * TZ;
@@ -1190,7 +1190,7 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
         else
             k_mic_lane2<REV, TY, TZ, 4, 0><<<(unsigned)tiles, TY * TZ + 32, 0, st>>>(B);
     }
-    return cudaGetLastError();
+    return cudaPeekAtLastError();
 }
 
 cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st) {
@@ -1202,6 +1202,7 @@ cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st) {
     LANE_CASE(32, 8)
     LANE_CASE(8, 8)
     LANE_CASE(32, 4)
+    LANE_CASE(32, 16)
 #undef LANE_CASE
     return rev ? launch_lane_shape<true, 16, 8>(A, st) : launch_lane_shape<false, 16, 8>(A, st);
 }
