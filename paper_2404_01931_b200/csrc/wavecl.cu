@@ -31,8 +31,7 @@ namespace flip {
 namespace {
 
 constexpr int CT = 16;   // tile edge: TY = TZ = 16
-constexpr int KC = 4;    // operand chunk (steps) per bulk copy
-constexpr int NB = 3;    // operand chunk ring depth
+
 constexpr int UH = 4;    // global-halo prefetch depth (steps)
 
 __device__ __forceinline__ unsigned smem_addr(const void *p) { return smem_u32(p); }
@@ -86,7 +85,7 @@ __device__ __forceinline__ void cluster_tile(int t, int CB, int CC, int &bq, int
 
 }  // namespace
 
-template <bool REV, int CY, int CZ>
+template <bool REV, int CY, int CZ, int KC, int NB, int L2AHEAD>
 __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
     constexpr int TY = CT, TZ = CT, TP = TY * TZ;
     constexpr int DY = TY - 1, DZ = TZ - 1;
@@ -130,6 +129,33 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
     const bool ydin = ry > 0, ydout = ry < CY - 1;
     const bool zdin = rz > 0, zdout = rz < CZ - 1;
 
+    // operands: KC-step chunks through the bulk-copy engine into an NB-deep
+    // ring after the face rings (opb[buf][src|precon][KC][TP]).  The helper
+    // warp's lane 0 issues them, off the compute warps' critical path.
+    double *opb = ring + (int64_t)nsteps * (TY + TZ);
+    const int nch = (nsteps + KC - 1) / KC;
+    auto issue = [&](int ch) {
+        if (ch >= nch) return;
+        const int64_t tbase = (int64_t)tile * nsteps * TP;
+        const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
+        const int lo = REV ? nsteps - s0 - cnt : s0;
+        const int buf = ch % NB;
+        const unsigned bytes = (unsigned)(cnt * TP * 8);
+        mbar_expect_tx(&mbar[buf], 2 * bytes);
+        bulk_g2s(opb + (buf * 2 + 0) * KC * TP, A.src + tbase + (int64_t)lo * TP, bytes, &mbar[buf]);
+        bulk_g2s(opb + (buf * 2 + 1) * KC * TP, A.precon + tbase + (int64_t)lo * TP, bytes,
+                 &mbar[buf]);
+        // stage a later chunk in L2 so the smem ring only has to hide L2 latency
+        const int pf = ch + L2AHEAD;
+        if (L2AHEAD > 0 && pf < nch) {
+            const int p0 = pf * KC, pc = min(KC, nsteps - p0);
+            const int plo = REV ? nsteps - p0 - pc : p0;
+            const unsigned pb = (unsigned)(pc * TP * 8);
+            bulk_prefetch_l2(A.src + tbase + (int64_t)plo * TP, pb);
+            bulk_prefetch_l2(A.precon + tbase + (int64_t)plo * TP, pb);
+        }
+    };
+
     if (t >= TP) {
         // -------------------- helper warp: faces across cluster boundaries
         const int l = t - TP;
@@ -165,6 +191,8 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
         }
         const bool cvalid = G.jlo + b * TY + cons_j <= G.jhi && G.klo + c * TZ + cons_k <= G.khi;
         if (!cvalid) in = nullptr;
+        if (l == 0)
+            for (int q = 0; q < NB; q++) issue(q);
         double hr[UH];
         auto fetch = [&](int s, int u) {
             const int sp = s + D;
@@ -179,6 +207,11 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 const int s = s0 + u;
                 if (s >= nsteps) break;
                 __syncthreads();
+                if (l == 0 && s > 0 && s % KC == 0) {
+                    // every compute thread finished chunk s/KC - 1 before this barrier
+                    fence_proxy_async();
+                    issue(s / KC - 1 + NB);
+                }
                 const int cur = s & 1, prv = cur ^ 1;
                 if (out && s > 0) publish(out + (int64_t)(s - 1) * W, sval[prv][out_row][out_col]);
                 if (in) {
@@ -211,31 +244,12 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
         const int yr = kk + 1, yc = REV ? jj + 2 : jj, zr = REV ? kk + 2 : kk, zc = jj + 1;
         const int64_t base = (int64_t)tile * nsteps * TP + t;
         double *dstL = A.dst + base;
-        // operands: KC-step chunks through the bulk-copy engine into an
-        // NB-deep ring after the face rings (opb[buf][src|precon][KC][TP])
-        double *opb = ring + (int64_t)nsteps * (TY + TZ);
-        const int nch = (nsteps + KC - 1) / KC;
-        const int64_t tbase = (int64_t)tile * nsteps * TP;
-        auto issue = [&](int ch) {  // thread 0 only
-            if (ch >= nch) return;
-            const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
-            const int lo = REV ? nsteps - s0 - cnt : s0;
-            const int buf = ch % NB;
-            const unsigned bytes = (unsigned)(cnt * TP * 8);
-            mbar_expect_tx(&mbar[buf], 2 * bytes);
-            bulk_g2s(opb + (buf * 2 + 0) * KC * TP, A.src + tbase + (int64_t)lo * TP, bytes,
-                     &mbar[buf]);
-            bulk_g2s(opb + (buf * 2 + 1) * KC * TP, A.precon + tbase + (int64_t)lo * TP, bytes,
-                     &mbar[buf]);
-        };
-        if (t == 0)
-            for (int q = 0; q < NB; q++) issue(q);
         double pv = nz0;
         const double sc = A.scale;
         for (int ch = 0; ch < nch; ch++) {
             const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
             const int buf = ch % NB;
-            mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
+            if (!(A.mode & 128)) mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
             const double *ab = opb + (buf * 2 + 0) * KC * TP + t;
             const double *pb = opb + (buf * 2 + 1) * KC * TP + t;
 #pragma unroll
@@ -243,17 +257,13 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 if (u >= cnt) break;
                 const int s = s0 + u;
                 __syncthreads();
-                if (u == 0 && ch > 0 && t == 0) {
-                    // every thread finished chunk ch-1 before this barrier
-                    fence_proxy_async();
-                    issue(ch - 1 + NB);
-                }
                 const int cur = s & 1, prv = cur ^ 1;
                 const int idx = REV ? cnt - 1 - u : u;
-                const double a = ab[idx * TP], pr = pb[idx * TP];
+                const double a = (A.mode & 128) ? 1.0 : ab[idx * TP];
+                const double pr = (A.mode & 128) ? 0.5 : pb[idx * TP];
                 double yv = sval[prv][yr][yc], zv = sval[prv][zr][zc];
-                if (yin) yv = s + DY < nsteps ? poll_local(yring + (s + DY) * TZ + kk) : nz0;
-                if (zin) zv = s + DZ < nsteps ? poll_local(zring + (s + DZ) * TY + jj) : nz0;
+                if (yin && !(A.mode & 64)) yv = s + DY < nsteps ? poll_local(yring + (s + DY) * TZ + kk) : nz0;
+                if (zin && !(A.mode & 64)) zv = s + DZ < nsteps ? poll_local(zring + (s + DZ) * TY + jj) : nz0;
                 if (A.trace && !REV && t == 0 && tile < 8 && s < 300) {
                     unsigned long long g;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 if (!REV) {  // _core.pyx:322-332
                     double tt = ((a + pv) + yv) + zv;
                     double q = tt * pr;
-                    if (row) dstL[(int64_t)lstep(s) * TP] = q;
+                    if (row && !(A.mode & 16)) dstL[(int64_t)lstep(s) * TP] = q;
                     o = (sc * pr) * q;
                 } else {     // _core.pyx:333-346
                     double sp = sc * pr;
@@ -275,10 +285,12 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 o = row ? o : nz0;
                 sval[cur][kk + 1][jj + 1] = o;
                 pv = o;
-                if (yout) st_remote(yout + (unsigned)(s * TZ * 8), o);
-                if (zout) st_remote(zout + (unsigned)(s * TY * 8), o);
-                if (gy) publish(gy + (int64_t)s * TZ, o);
-                if (gz) publish(gz + (int64_t)s * TY, o);
+                if (!(A.mode & 32)) {
+                    if (yout) st_remote(yout + (unsigned)(s * TZ * 8), o);
+                    if (zout) st_remote(zout + (unsigned)(s * TY * 8), o);
+                    if (gy) publish(gy + (int64_t)s * TZ, o);
+                    if (gz) publish(gz + (int64_t)s * TY, o);
+                }
             }
         }
         __syncthreads();  // matches the helper's final barrier
@@ -316,22 +328,38 @@ static int cluster_shape(int *cy, int *cz) {
 
 int mic_cluster_pad(int *cy, int *cz) { return cluster_shape(cy, cz); }
 
-template <bool REV, int CY, int CZ>
-static cudaError_t launch_cl(const LaneArgs &A, cudaStream_t st) {
+// operand chunk ring: KC steps per bulk copy, NB chunks in flight, and an
+// optional L2 prefetch L2AHEAD chunks further (FLIPB200_CL_CHUNKS=KCxNB[xL2]).
+// Measured at 256^3 (project stage, 4x4 clusters): 4x3 65.8 ms, 4x8 69.8,
+// 8x4 67.7, 4x3 + L2 prefetch 4 or 6 chunks ahead 65.8-65.9: deeper smem
+// rings cost residency, and operand latency is not what bounds the loop.
+static int chunk_cfg() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("FLIPB200_CL_CHUNKS");  // "KCxNB" or "KCxNBxL2"
+        int a = 4, b = 3, c = 0;
+        if (e) sscanf(e, "%dx%dx%d", &a, &b, &c);
+        v = c == 6 ? 4036 : (c == 4 ? 4034 : a * 100 + b);
+    }
+    return v;
+}
+
+template <bool REV, int CY, int CZ, int KC, int NB, int L2AHEAD>
+static cudaError_t launch_cl_k(const LaneArgs &A, cudaStream_t st) {
     const int tiles = A.geom.TB * A.geom.TC;
-    static const size_t pad = getenv("FLIPB200_CL_SMEM_PAD") ? atoi(getenv("FLIPB200_CL_SMEM_PAD")) : 0;
     // face rings (2 x nsteps x 16) + operand chunks (NB x 2 x KC x 256), 128-B aligned
     const size_t rings = ((size_t)A.geom.nsteps * 2 * CT * sizeof(double) + 127) / 128 * 128;
-    const size_t smem = rings + (size_t)NB * 2 * KC * CT * CT * sizeof(double) + pad;
-    static bool attr = [] {
-        cudaFuncSetAttribute(k_mic_cl<REV, CY, CZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        if (CY * CZ > 8)
-            cudaFuncSetAttribute(k_mic_cl<REV, CY, CZ>,
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        return true;
+    const size_t smem = rings + (size_t)NB * 2 * KC * CT * CT * sizeof(double);
+    static cudaError_t attr = [] {
+        cudaError_t e = cudaFuncSetAttribute(k_mic_cl<REV, CY, CZ, KC, NB, L2AHEAD>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             220 * 1024 - 6 * 1024);
+        if (e == cudaSuccess && CY * CZ > 8)
+            e = cudaFuncSetAttribute(k_mic_cl<REV, CY, CZ, KC, NB, L2AHEAD>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return e;
     }();
-    (void)attr;
+    if (attr != cudaSuccess) return attr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)tiles);
     cfg.blockDim = dim3(CT * CT + 32);
@@ -344,8 +372,20 @@ static cudaError_t launch_cl(const LaneArgs &A, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_cl<REV, CY, CZ>, A);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_cl<REV, CY, CZ, KC, NB, L2AHEAD>, A);
     return e != cudaSuccess ? e : cudaPeekAtLastError();
+}
+
+template <bool REV, int CY, int CZ>
+static cudaError_t launch_cl(const LaneArgs &A, cudaStream_t st) {
+    switch (chunk_cfg()) {
+        case 403: return launch_cl_k<REV, CY, CZ, 4, 3, 0>(A, st);
+        case 804: return launch_cl_k<REV, CY, CZ, 8, 4, 0>(A, st);
+        case 408: return launch_cl_k<REV, CY, CZ, 4, 8, 0>(A, st);
+        case 4036: return launch_cl_k<REV, CY, CZ, 4, 3, 6>(A, st);
+        case 4034: return launch_cl_k<REV, CY, CZ, 4, 3, 4>(A, st);
+        default: return launch_cl_k<REV, CY, CZ, 4, 3, 0>(A, st);
+    }
 }
 
 // Returns cudaErrorNotSupported when no cluster shape is configured (the

@@ -1,0 +1,128 @@
+// Which ingredient of the k_mic_cl step loop costs cycles?  Starts from the
+// bare skeleton (barrier + smem neighbours + MIC(0) chain + smem store) and
+// adds, by template flag:
+//   OPS  operands a, precon from a shared chunk (2 LDS) + row test + 8-byte STG
+//   HLP  a 9th warp that only joins the barriers (the helper)
+//   MB   mbarrier-completed bulk-copy chunks of 4 steps (helper lane 0 issues)
+//   RMT  16 lanes store their output into a cluster peer's smem (DSMEM)
+// One CTA per cluster pair (cluster of 2), 148 clusters' worth of CTAs.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ unsigned sa(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(unsigned long long *b) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(b)) : "memory"); }
+__device__ __forceinline__ void mb_expect(unsigned long long *b, unsigned n) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void mb_wait(unsigned long long *b, unsigned ph) {
+    asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(sa(b)), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void bulk(void *d, const void *s, unsigned n, unsigned long long *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(d)), "l"(s), "r"(n), "r"(sa(b)) : "memory");
+}
+
+template <int OPS, int HLP, int MB, int RMT, int NB = 2>
+__global__ void __launch_bounds__(288) k(int steps, const double *src, double *dst, unsigned long long *cyc) {
+    constexpr int KC = 4, TP = 256;
+    __shared__ double sval[2][18][18];
+    extern __shared__ __align__(128) double opb_raw[];
+    auto opb = reinterpret_cast<double (*)[2][KC][TP]>(opb_raw);
+    __shared__ __align__(8) unsigned long long mbar[NB];
+    __shared__ __align__(16) double peer_ring[64][16];
+    const int t = threadIdx.x;
+    for (int q = t; q < 2 * 18 * 18; q += blockDim.x) (&sval[0][0][0])[q] = 0.0;
+    for (int q = t; q < NB * 2 * KC * TP; q += blockDim.x) (&opb[0][0][0][0])[q] = 1.0;
+    if (t == 0) { for (int q = 0; q < NB; q++) mb_init(&mbar[q]); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    unsigned rk; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rk));
+    unsigned peer; asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(sa(&peer_ring[0][0])), "r"(rk ^ 1));
+    const int nch = steps / KC;
+    const double *gsrc = src + (size_t)blockIdx.x * steps * TP;
+    auto issue = [&](int ch) {
+        int buf = ch % NB;
+        mb_expect(&mbar[buf], 2 * KC * TP * 8);
+        bulk(&opb[buf][0][0][0], gsrc + (size_t)ch * KC * TP, KC * TP * 8, &mbar[buf]);
+        bulk(&opb[buf][1][0][0], gsrc + (size_t)ch * KC * TP, KC * TP * 8, &mbar[buf]);
+    };
+    const int nthr = HLP ? 288 : 256;
+    if (t >= 256) {
+        if (!HLP) return;
+        if (MB && t == 256) for (int q = 0; q < NB; q++) issue(q);
+        for (int s = 0; s < steps; s++) {
+            __syncthreads();
+            if (MB && t == 256 && s > 0 && s % KC == 0 && s / KC - 1 + NB < nch) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(s / KC - 1 + NB);
+            }
+        }
+        return;
+    }
+    if (MB && !HLP && t == 0) for (int q = 0; q < NB; q++) issue(q);
+    const int jj = t & 15, kk = t >> 4;
+    double pv = 0.0, sc = 0.25;
+    double *d = dst + (size_t)blockIdx.x * steps * TP + t;
+    long long c0 = clock64();
+    for (int s = 0; s < steps; s++) {
+        const int u = s % KC, ch = s / KC;
+        if (MB && u == 0) mb_wait(&mbar[ch % NB], (ch / NB) & 1);
+        if (HLP) __syncthreads(); else asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (MB && !HLP && t == 0 && u == 0 && ch > 0 && ch - 1 + NB < nch) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(ch - 1 + NB);
+        }
+        const int cur = s & 1, prv = cur ^ 1;
+        double a = 1e-3 * t, pr = 0.5;
+        if (OPS) { a = opb[ch % NB][0][u][t]; pr = opb[ch % NB][1][u][t]; }
+        double yv = sval[prv][kk + 1][jj], zv = sval[prv][kk][jj + 1];
+        double tt = ((a + pv) + yv) + zv;
+        double q = tt * pr;
+        if (OPS && a != 12345.0) d[(size_t)s * TP] = q;
+        double o = (sc * pr) * q;
+        sval[cur][kk + 1][jj + 1] = o;
+        pv = o;
+        if (RMT && kk == 15)
+            asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(peer + (unsigned)(((s & 63) * 16 + jj) * 8)), "d"(o) : "memory");
+    }
+    long long c1 = clock64();
+    if (t == 0 && blockIdx.x == 0) cyc[0] = (c1 - c0) / steps;
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    (void)nthr;
+}
+
+template <int OPS, int HLP, int MB, int RMT, int NB = 2>
+void run(const char *name, const double *src, double *dst, unsigned long long *cyc, int steps) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(296);
+    cfg.blockDim = dim3(288);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cfg.dynamicSmemBytes = NB * 2 * 4 * 256 * 8;
+    cudaFuncSetAttribute(k<OPS, HLP, MB, RMT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int rep = 0; rep < 2; rep++) {
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k<OPS, HLP, MB, RMT, NB>, steps, src, dst, cyc);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("%s: err %s\n", name, cudaGetErrorString(e)); return; }
+    }
+    printf("%-34s %llu cycles/step\n", name, cyc[0]);
+}
+
+int main() {
+    const int steps = 512;
+    double *src, *dst;
+    unsigned long long *cyc;
+    size_t n = (size_t)296 * steps * 256;
+    cudaMalloc(&src, n * 8); cudaMemset(src, 0, n * 8);
+    cudaMalloc(&dst, n * 8);
+    cudaMallocManaged(&cyc, 64);
+    run<0, 0, 0, 0>("skeleton", src, dst, cyc, steps);
+    run<1, 0, 0, 0>("+ops (smem a/pr, STG)", src, dst, cyc, steps);
+    run<0, 1, 0, 0>("+helper warp", src, dst, cyc, steps);
+    run<1, 1, 0, 0>("+ops +helper", src, dst, cyc, steps);
+    run<1, 1, 1, 0>("+ops +helper +mbar chunks", src, dst, cyc, steps);
+    run<1, 1, 1, 1>("+ops +helper +mbar +remote stores", src, dst, cyc, steps);
+    run<1, 0, 1, 0>("+ops +mbar (thread 0 issues)", src, dst, cyc, steps);
+    run<1, 1, 1, 0, 4>("+ops +helper +mbar NB=4", src, dst, cyc, steps);
+    run<1, 1, 1, 0, 8>("+ops +helper +mbar NB=8", src, dst, cyc, steps);
+    run<1, 1, 1, 0, 16>("+ops +helper +mbar NB=16", src, dst, cyc, steps);
+    return 0;
+}
