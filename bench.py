@@ -338,13 +338,13 @@ def run_ours(args):
         alg = pbytes.value / plaunch.value
         achieved = alg / (avg_ms / 1e3) / 1e9
         tr = load_traffic()
-        roof = {"bound": "hbm", "kernel": "k_mic_lane2 (MIC(0) substitution wavefront, fwd+bwd)",
+        roof = {"bound": "hbm", "kernel": "k_mic_cl (MIC(0) substitution wavefront, DSMEM clusters, fwd+bwd)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
                 "avg_launch_ms": avg_ms, "launches_timed": int(plaunch.value),
                 "share_of_step": pms.value / ms,
                 # the ncu capture is of the 256^3 dam-break sweep
-                "traffic": ((tr or {}).get("k_mic_lane2_dram_bytes_per_launch")
+                "traffic": ((tr or {}).get("k_mic_cl_dram_bytes_per_launch")
                             if (args.res, args.scene) == (256, "dam-break") else None),
                 "note": "latency-bound dependency wavefront (see DESIGN.md); "
                         "frac is of the HBM copy peak"}
