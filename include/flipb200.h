@@ -159,6 +159,12 @@ int flip_get_known(flip_ctx *ctx, uint8_t *ku, uint8_t *kv, uint8_t *kw);
  * (region order, covered cells ascending, subcells ascending) to the
  * particle set.  Mark the shell with flip_set_solid_shell first. */
 int flip_set_solid_shell(flip_ctx *ctx);
+/* Scene extension (BASELINE config 4): mark the cells
+ * [i0,i1] x [j0,j1] x [k0,k1] (inclusive, clipped to the grid) SOLID.  The
+ * reference has only the wall shell; every stage already honours arbitrary
+ * SOLID labels, so obstacles are labels injected after the shell. */
+int flip_set_solid_box(flip_ctx *ctx, int64_t i0, int64_t i1, int64_t j0, int64_t j1,
+                       int64_t k0, int64_t k1);
 int flip_seed_regions(flip_ctx *ctx, int32_t nregions, const flip_region *regions,
                       uint64_t rng_seed);
 

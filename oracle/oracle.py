@@ -28,7 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 SOLID, FLUID, AIR = 0, 1, 2
-SCENE_NAMES = ("dam-break", "double-dam-break", "water-drop")
+SCENE_NAMES = ("dam-break", "double-dam-break", "water-drop", "double-dam-break-obstacle")
 SOLVER_KIND = {"jacobi": 0, "gs": 1, "rbgs": 2, "pcg": 3}
 PRECOND = {"mic0": 0, "jacobi": 1, "none": 2}
 STAGES = ("dt_compute", "advect", "bin", "classify", "p2g", "force", "project",
@@ -160,6 +160,7 @@ class Spec:
     extrapolation_layers: int = 2
     steps: int = 50
     precond: str = "mic0"   # not in SceneSpec; the reference hard-wires mic0 (pressure.py:274)
+    obstacles: tuple = ()   # extension: SOLID cell boxes after the shell
 
     def resolved_max_iters(self) -> int:
         if self.max_iters is not None:
@@ -243,7 +244,7 @@ def scene_regions(spec: Spec, dims: Dimz):                    # sim.py:140-201
         else:
             rho, cx, cy = spec.density, max(1, round(0.25 * ni)), max(1, round(0.75 * nj))
         return [_box_region(dims, lo_c, lo_c + cx - 1, lo_c, lo_c + cy - 1, lo_c, hi_c, rho)]
-    if spec.name == "double-dam-break":
+    if spec.name in ("double-dam-break", "double-dam-break-obstacle"):
         if spec.particle_target:
             rho, cx, cy = _fit_box(spec.particle_target // 2, ni, nj, nk, 0.25, 0.75)
         else:
@@ -315,6 +316,28 @@ def empty_grid(dims: Dimz):
             np.full(nx * ny * nz, AIR, dtype=np.uint8))
 
 
+def scene_obstacles(spec: Spec, dims: Dimz):
+    """Extension (no reference counterpart): SOLID boxes of the scene, same
+    rule as paper_2404_01931_b200.sim.scene_obstacles."""
+    boxes = [tuple(int(x) for x in b) for b in spec.obstacles]
+    if spec.name == "double-dam-break-obstacle":
+        lo_c, hi_c = 1, spec.res - 2
+        n = hi_c - lo_c + 1
+        i0 = lo_c + round(0.45 * n)
+        i1 = max(i0, lo_c + round(0.55 * n) - 1)
+        j1 = lo_c + max(1, round(0.35 * n)) - 1
+        k0 = lo_c + round(0.25 * n)
+        k1 = max(k0, lo_c + round(0.75 * n) - 1)
+        boxes.append((i0, i1, lo_c, j1, k0, k1))
+    return boxes
+
+
+def solid_boxes(dims: Dimz, label: np.ndarray, boxes) -> None:
+    lab = label.reshape(dims.nz, dims.ny, dims.nx)
+    for i0, i1, j0, j1, k0, k1 in boxes:
+        lab[max(k0, 0):k1 + 1, max(j0, 0):j1 + 1, max(i0, 0):i1 + 1] = SOLID
+
+
 def solid_shell(dims: Dimz, label: np.ndarray) -> None:       # grid.py:110-118
     lab = label.reshape(dims.nz, dims.ny, dims.nx)
     lab[0] = SOLID
@@ -376,6 +399,7 @@ def make_scene(spec: Spec, rng_seed: int = 0) -> OState:      # sim.py:204-223
     dims = Dimz(spec.res, spec.res, spec.res, 1.0 / spec.res)
     u, v, w, p, label = empty_grid(dims)
     solid_shell(dims, label)
+    solid_boxes(dims, label, scene_obstacles(spec, dims))
     regions = scene_regions(spec, dims)
     parts = [np.zeros(0) for _ in range(6)]
     for region in regions:

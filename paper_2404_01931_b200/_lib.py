@@ -125,6 +125,8 @@ _SIGNATURES = {
     "flip_set_known": (C.c_int, [_vp, _u8, _u8, _u8]),
     "flip_get_known": (C.c_int, [_vp, _u8, _u8, _u8]),
     "flip_set_solid_shell": (C.c_int, [_vp]),
+    "flip_set_solid_box": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                     C.c_int64, C.c_int64]),
     "flip_seed_regions": (C.c_int, [_vp, C.c_int32, C.POINTER(Region), C.c_uint64]),
     "flip_step": (C.c_int, [_vp, C.POINTER(StepParams), C.POINTER(StepReportC)]),
     "flip_run_stages": (C.c_int, [_vp, C.POINTER(StepParams), C.c_int32, C.c_int32,

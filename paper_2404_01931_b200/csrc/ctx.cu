@@ -463,6 +463,23 @@ extern "C" int flip_set_solid_shell(flip_ctx *c) {
     return flip_synchronize(c);
 }
 
+extern "C" int flip_set_solid_box(flip_ctx *c, int64_t i0, int64_t i1, int64_t j0, int64_t j1,
+                                  int64_t k0, int64_t k1) {
+    cudaSetDevice(c->device);
+    const int64_t n[3] = {c->d.nx, c->d.ny, c->d.nz};
+    int64_t lo[3] = {i0, j0, k0}, hi[3] = {i1, j1, k1};
+    int b[6];
+    for (int a = 0; a < 3; a++) {
+        lo[a] = lo[a] < 0 ? 0 : lo[a];
+        hi[a] = hi[a] > n[a] - 1 ? n[a] - 1 : hi[a];
+        if (lo[a] > hi[a]) return 0;  // empty after clipping
+        b[2 * a] = (int)lo[a];
+        b[2 * a + 1] = (int)hi[a];
+    }
+    launch_set_solid_box(*c, b);
+    return flip_synchronize(c);
+}
+
 extern "C" int flip_seed_regions(flip_ctx *c, int32_t nregions, const flip_region *regions,
                                  uint64_t rng_seed) {
     cudaSetDevice(c->device);

@@ -115,6 +115,7 @@ void stage_apply_gradient(Ctx &c, const flip_step_params &prm);
 void stage_g2p(Ctx &c, const flip_step_params &prm);
 void stage_reseed(Ctx &c, const flip_step_params &prm);
 void launch_particle_cells(Ctx &c, int *out);
+void launch_set_solid_box(Ctx &c, const int b[6]);
 
 void launch_set_solid_shell(Ctx &c);
 int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed);

@@ -331,6 +331,20 @@ __global__ void k_solid_shell(uint8_t *label, Dims d) {
     }
 }
 
+__global__ void k_solid_box(uint8_t *label, Dims d, int i0, int i1, int j0, int j1, int k0, int k1) {
+    int64_t nc = d.ncells();
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((int64_t)d.nx * d.ny));
+        if (i >= i0 && i <= i1 && j >= j0 && j <= j1 && k >= k0 && k <= k1) label[c] = SOLID;
+    }
+}
+
+void launch_set_solid_box(Ctx &c, const int b[6]) {
+    k_solid_box<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.d, b[0], b[1], b[2], b[3],
+                                                           b[4], b[5]);
+    c.launches++;
+}
+
 void launch_set_solid_shell(Ctx &c) {
     k_solid_shell<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.d);
     c.launches++;

@@ -22,7 +22,7 @@ from .errors import ConfigError, SingularSystemError, SolverBreakdownError, Solv
 from .grid import AIR, FLUID, SOLID, GridDims, MacGrid, interior_box_from_labels
 from .particles import ParticleSet, SeedRegion, covered_cells
 
-SCENE_NAMES = ("dam-break", "double-dam-break", "water-drop")
+SCENE_NAMES = ("dam-break", "double-dam-break", "water-drop", "double-dam-break-obstacle")
 SOLVERS = ("jacobi", "gs", "rbgs", "pcg")
 PRECONDITIONERS = ("mic0", "jacobi", "none")
 
@@ -78,6 +78,9 @@ class SceneSpec:
     extrapolation_layers: int = 2
     steps: int = 50
     precond: str = "mic0"
+    # scene extension: extra SOLID cell boxes
+    # (i0, i1, j0, j1, k0, k1), inclusive, applied after the wall shell
+    obstacles: tuple = ()
 
     def resolved_max_iters(self) -> int:
         if self.max_iters is not None:
@@ -135,6 +138,27 @@ def _box(dims, i0, i1, j0, j1, k0, k1, density):
                           o + np.array([i1 + 1, j1 + 1, k1 + 1]) * dims.dtau, density)
 
 
+def scene_obstacles(spec: SceneSpec, dims: GridDims) -> list:
+    """SOLID cell boxes of the scene: ``spec.obstacles`` plus, for
+    "double-dam-break-obstacle", a pillar between the two dams (x 45-55%,
+    y floor-35%, z 25-75% of the interior).  Extension: the reference scenes
+    have only the wall shell (BASELINE config 4)."""
+    boxes = [tuple(int(x) for x in b) for b in spec.obstacles]
+    if spec.name == "double-dam-break-obstacle":
+        lo_c, hi_c = 1, spec.res - 2
+        n = hi_c - lo_c + 1
+        i0 = lo_c + round(0.45 * n)
+        i1 = max(i0, lo_c + round(0.55 * n) - 1)
+        j1 = lo_c + max(1, round(0.35 * n)) - 1
+        k0 = lo_c + round(0.25 * n)
+        k1 = max(k0, lo_c + round(0.75 * n) - 1)
+        boxes.append((i0, i1, lo_c, j1, k0, k1))
+    for b in boxes:
+        if len(b) != 6:
+            raise ConfigError(f"obstacle box needs 6 inclusive cell bounds, got {b}")
+    return boxes
+
+
 def scene_regions(spec: SceneSpec, dims: GridDims) -> list:
     """Seed regions of the named scene (sim.py:140-201)."""
     lo_c, hi_c = 1, spec.res - 2          # one-cell solid shell
@@ -144,8 +168,8 @@ def scene_regions(spec: SceneSpec, dims: GridDims) -> list:
     edge = dims.nx * dims.dtau
     o = np.asarray(dims.origin, dtype=np.float64)
     tgt = spec.particle_target
-    if spec.name in ("dam-break", "double-dam-break"):
-        double = spec.name == "double-dam-break"
+    if spec.name in ("dam-break", "double-dam-break", "double-dam-break-obstacle"):
+        double = spec.name != "dam-break"
         if tgt:
             rho, cx, cy = _fit_box(tgt // 2 if double else tgt, ni, nj, nk, 0.25, 0.75)
         else:
@@ -216,6 +240,8 @@ def make_scene(spec: SceneSpec, rng_seed: int = 0, device: int = 0,
     regions = scene_regions(spec, dims)
     dev = Device(dims, capacity=capacity, device=device)
     check(LIB.flip_set_solid_shell(dev.ctx), "flip_set_solid_shell")
+    for b in scene_obstacles(spec, dims):
+        check(LIB.flip_set_solid_box(dev.ctx, *b), "flip_set_solid_box")
     arr = (_lib.Region * len(regions))(*[r.to_c() for r in regions])
     check(LIB.flip_seed_regions(dev.ctx, len(regions), arr, int(rng_seed) & rng.MASK64),
           "flip_seed_regions")

@@ -36,6 +36,11 @@ CASES = [
     dict(name="dam-break", res=32, solver="pcg", seed=0, steps=3),
     dict(name="dam-break", res=12, solver="pcg", seed=2, steps=2, gravity=(0.0, 0.0, 0.0)),
     dict(name="double-dam-break", res=20, solver="pcg", seed=7, steps=3, flip_fraction=0.0),
+    # scene extension: the reference scene with SOLID boxes
+    # injected into its labels after make_scene (the seeding never touches them)
+    dict(name="double-dam-break-obstacle", res=20, solver="pcg", seed=2, steps=3),
+    dict(name="dam-break", res=16, solver="jacobi", seed=4, steps=2,
+         obstacles=((8, 10, 1, 5, 4, 11),)),
 ]
 
 
@@ -69,9 +74,20 @@ def main():
 
     steps_out = {}
     for c in CASES:
-        kw = {k: v for k, v in c.items() if k not in ("seed", "steps")}
+        kw = {k: v for k, v in c.items() if k not in ("seed", "steps", "obstacles")}
+        boxes = []
+        if kw["name"] == "double-dam-break-obstacle" or c.get("obstacles"):
+            import oracle as O
+            boxes = O.scene_obstacles(O.Spec(**{k: v for k, v in c.items()
+                                                if k not in ("seed", "steps")}), None)
+            if kw["name"] == "double-dam-break-obstacle":
+                kw["name"] = "double-dam-break"
         spec = RS.SceneSpec(**kw)
         st = RS.make_scene(spec, rng_seed=c["seed"])
+        if boxes:
+            lab = st.grid.label3()
+            for i0, i1, j0, j1, k0, k1 in boxes:
+                lab[k0:k1 + 1, j0:j1 + 1, i0:i1 + 1] = 0      # SOLID (grid.py:17)
         rec = {"density": spec.density, "states": [ref_state_digests(st)], "reports": []}
         for _ in range(c["steps"]):
             r = RS.step(st, spec)

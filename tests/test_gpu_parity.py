@@ -22,6 +22,8 @@ STEP_CASES = [
     dict(name="water-drop", res=20, solver="pcg", particle_target=20000),
     dict(name="dam-break", res=20, solver="pcg", precond="jacobi"),
     dict(name="double-dam-break", res=18, solver="pcg", precond="none", flip_fraction=0.0),
+    dict(name="double-dam-break-obstacle", res=24, solver="pcg"),
+    dict(name="water-drop", res=20, solver="rbgs", obstacles=((3, 6, 1, 3, 3, 16), (12, 14, 2, 8, 5, 9))),
 ]
 
 
