@@ -144,6 +144,12 @@ int flip_set_particles(flip_ctx *ctx, int64_t n, const double *px, const double 
 int flip_get_particles(flip_ctx *ctx, double *px, double *py, double *pz, double *vx,
                        double *vy, double *vz);
 int flip_particle_count(flip_ctx *ctx, int64_t *n);
+/* FLIP v1 snapshot payload (io.py:23-55): the six particle arrays as
+ * float32 SoA (out[6 * n], host), converted on the device with
+ * round-to-nearest (numpy astype('<f4')); and the reverse, widening exactly
+ * (the set is unbinned afterwards, as with flip_set_particles). */
+int flip_get_particles_f32(flip_ctx *ctx, float *out_soa);
+int flip_set_particles_f32(flip_ctx *ctx, int64_t n, const float *in_soa);
 /* SpaceHash: offset/count int64[ncells]; uploading sets the binned hash. */
 int flip_set_hash(flip_ctx *ctx, const int64_t *offset, const int64_t *count);
 int flip_get_hash(flip_ctx *ctx, int64_t *offset, int64_t *count);

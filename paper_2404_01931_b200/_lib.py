@@ -117,6 +117,8 @@ _SIGNATURES = {
     "flip_set_particles": (C.c_int, [_vp, C.c_int64, _d, _d, _d, _d, _d, _d]),
     "flip_get_particles": (C.c_int, [_vp, _d, _d, _d, _d, _d, _d]),
     "flip_particle_count": (C.c_int, [_vp, _i64]),
+    "flip_get_particles_f32": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "flip_set_particles_f32": (C.c_int, [_vp, C.c_int64, C.POINTER(C.c_float)]),
     "flip_set_hash": (C.c_int, [_vp, _i64, _i64]),
     "flip_get_hash": (C.c_int, [_vp, _i64, _i64]),
     "flip_get_fluid_cells": (C.c_int, [_vp, _i64, _i64]),

@@ -102,7 +102,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
                     c->has_air, c->cell_of_row, c->nbr, c->diagd, c->rhs, c->x, c->r, c->z, c->s,
                     c->q, c->tq, c->precon, c->xtmp, c->u64_scratch, c->lvl, c->lvl_rows,
-                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->lrow, c->posL, c->laneA, c->laneB, c->laneC, c->laneD, c->sc};
+                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->lrow, c->posL, c->laneA, c->laneB, c->laneC, c->laneD, c->sc, c->f32_buf};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
@@ -376,6 +376,45 @@ extern "C" int flip_particle_cells(flip_ctx *c, int32_t *cells_dev) {
     launch_particle_cells(*c, cells_dev);
     FLIP_CUDA_OK(cudaGetLastError());
     return 0;
+}
+
+// f32 staging for snapshots: allocated on first use, grown on demand, freed
+// by flip_destroy.
+static int f32_stage(flip_ctx *c, int64_t n, float **buf) {
+    const size_t need = sizeof(float) * 6 * (size_t)(n > 0 ? n : 1);
+    if (c->f32_cap < need) {
+        if (c->f32_buf) cudaFree(c->f32_buf);
+        c->f32_buf = nullptr;
+        c->f32_cap = 0;
+        FLIP_CUDA_OK(cudaMalloc(&c->f32_buf, need));
+        c->f32_cap = need;
+    }
+    *buf = (float *)c->f32_buf;
+    return 0;
+}
+
+extern "C" int flip_get_particles_f32(flip_ctx *c, float *out) {
+    cudaSetDevice(c->device);
+    float *buf;
+    TRY(f32_stage(c, c->n, &buf));
+    launch_particles_f32(*c, buf, true);
+    TRY(d2h(out, buf, sizeof(float) * 6 * c->n, c->st));
+    return flip_synchronize(c);
+}
+
+extern "C" int flip_set_particles_f32(flip_ctx *c, int64_t n, const float *in) {
+    cudaSetDevice(c->device);
+    if (n < 0 || n > c->cap) {
+        set_error("particle count exceeds capacity");
+        return FLIP_E_CAPACITY;
+    }
+    float *buf;
+    TRY(f32_stage(c, n, &buf));
+    TRY(h2d(buf, in, sizeof(float) * 6 * n, c->st));
+    c->n = n;
+    c->keys_valid = 0;
+    launch_particles_f32(*c, buf, false);
+    return flip_synchronize(c);
 }
 
 extern "C" int flip_particle_count(flip_ctx *c, int64_t *n) {

@@ -50,6 +50,8 @@ struct Ctx {
     int64_t cap = 0;        // particle capacity
     int64_t n = 0;          // particle count (host mirror)
     int64_t slab_c0 = 0, slab_c1 = -1;  // reseed cell range (flip_set_slab); -1: all
+    void *f32_buf = nullptr;           // snapshot staging (flip_*_particles_f32)
+    size_t f32_cap = 0;
     ParticlePtrs P{}, Q{};  // current and back particle buffers
     double *u = nullptr, *v = nullptr, *w = nullptr, *p = nullptr;
     uint8_t *label = nullptr;
@@ -116,6 +118,7 @@ void stage_g2p(Ctx &c, const flip_step_params &prm);
 void stage_reseed(Ctx &c, const flip_step_params &prm);
 void launch_particle_cells(Ctx &c, int *out);
 void launch_set_solid_box(Ctx &c, const int b[6]);
+void launch_particles_f32(Ctx &c, float *buf, bool to_f32);
 
 void launch_set_solid_shell(Ctx &c);
 int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed);

@@ -209,6 +209,24 @@ void launch_sample_many(const Dims &d, const double *u, const double *v, const d
     k_sample_many<<<nblocks(n), kThreads, 0, st>>>(d, u, v, w, n, px, py, pz, vx, vy, vz);
 }
 
+// FLIP v1 snapshot payload (io.py:23-55): f64 SoA <-> f32 SoA
+__global__ void k_to_f32(ParticlePtrs P, int64_t n, float *__restrict__ out) {
+    for (int64_t t = gtid(); t < n; t += gstride())
+#pragma unroll
+        for (int a = 0; a < 6; a++) out[a * n + t] = __double2float_rn(P.a[a][t]);
+}
+__global__ void k_from_f32(ParticlePtrs P, int64_t n, const float *__restrict__ in) {
+    for (int64_t t = gtid(); t < n; t += gstride())
+#pragma unroll
+        for (int a = 0; a < 6; a++) P.a[a][t] = (double)in[a * n + t];
+}
+void launch_particles_f32(Ctx &c, float *buf, bool to_f32) {
+    if (c.n <= 0) return;
+    if (to_f32) k_to_f32<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, buf);
+    else k_from_f32<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, buf);
+    c.launches++;
+}
+
 // cell_index_many of the current particles (flip_particle_cells)
 __global__ void k_particle_cells(ParticlePtrs P, int64_t n, Dims d, int *__restrict__ out) {
     for (int64_t t = gtid(); t < n; t += gstride()) out[t] = cell_of(d, P.a[0][t], P.a[1][t], P.a[2][t]);
