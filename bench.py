@@ -237,11 +237,13 @@ def run_ours(args):
     launches = 0
     stage = {}
     iters = []
+    rows_acc = []
     for _ in range(args.steps):
         parts += st.particles.count
         rep = do_step(st, spec)
         launches += rep.gpu_launches
         iters.append(rep.solver_iterations)
+        rows_acc.append(rep.nrows)
         for k, v in rep.timings.as_dict().items():
             stage[k] = stage.get(k, 0.0) + v
     e1.record(stream)
@@ -330,6 +332,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
+    mean_rows = sum(rows_acc) / max(len(rows_acc), 1)
     # ---------------- roofline of the dominant kernel ----------------
     peak, peak_kind = measured_peak()
     roof = None
@@ -361,6 +364,23 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
                    "sample": f"failed: {exc}"}
 
+    # whole-step HBM roofline: algorithmic bytes of every
+    # stage, with this run's particle count, rows and solver iterations
+    res = args.res
+    C_ = float(res ** 3)
+    F_ = 3.0 * (res + 1) * res * res
+    N_ = float(total_parts) / args.steps     # global particles entering a step
+    R_ = float(mean_rows) if mean_rows else 0.0
+    its = sum(iters) / max(len(iters), 1)
+    per_it = 147.0 * R_ if args.solver == "pcg" else 25.0 * R_
+    step_bytes = (24 * N_ + 72 * N_ + (96 * N_ + 8 * C_) + 6 * C_ + (48 * N_ + 8 * C_ + 17 * F_)
+                  + (16 * F_ + C_) + (8 * F_ + C_ + 9 * R_) + its * per_it + 17 * R_
+                  + (18 * C_ + 66 * F_) + (72 * N_ + 16 * F_) + (96 * N_ + 8 * C_))
+    step_gbs = step_bytes / (ms_max / args.steps / 1e3) / 1e9
+    roof_step = {"alg_bytes_per_step": step_bytes, "achieved": step_gbs, "unit": "GB/s",
+                 "peak": peak, "frac": step_gbs / peak,
+                 "formula": "SURVEY 8(d) per-stage algorithmic bytes, N/R/iterations measured"}
+
     line = {"metric": BASE_METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": warm, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
@@ -370,6 +390,7 @@ def run_ours(args):
                            parallelism=(f"slab-z{world}: particle stages sharded, grid stages "
                                         "and MIC(0)-PCG replicated" if world > 1 else "single")),
             "clocks": clk, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+            "roofline_step": roof_step,
             "cpu_baseline": cpu,
             "detail": {"stage_ms_mean": {k: v / args.steps for k, v in stage.items()},
                        "solver_iterations": iters,
