@@ -75,6 +75,55 @@ __device__ __forceinline__ void uf_unite(int *par, int a, int b) {
     } while (repeat);
 }
 
+// Parent of each FLUID cell = the first cell of its x-run (one warp per
+// x-row, ballots with a carry across 32-cell chunks): the x links of the
+// union-find come for free, no atomics.  The run start is the run's lowest
+// cell, consistent with union by smaller root.
+__global__ void k_uf_runs(const uint8_t *__restrict__ label, Dims d, int *par,
+                          uint8_t *has_air) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nrow = (int64_t)d.ny * d.nz;
+    const int64_t w0 = (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = w0; row < nrow; row += nw) {
+        const int64_t base = row * d.nx;
+        int carry = -1;  // start of the run reaching the chunk's first cell
+        for (int x0 = 0; x0 < d.nx; x0 += 32) {
+            const int x = x0 + lane;
+            const bool in = x < d.nx;
+            const bool fl = in && label[base + x] == FLUID;
+            const unsigned notfl = __ballot_sync(0xffffffffu, !fl);
+            const unsigned upto = notfl & (0xffffffffu >> (31 - lane));  // lanes <= me
+            int start;
+            if (upto) start = x0 + (31 - __clz(upto)) + 1;  // after the last non-fluid
+            else start = carry >= 0 ? carry : x0;
+            if (in) {
+                par[base + x] = fl ? (int)(base + start) : -1;
+                has_air[base + x] = 0;
+            }
+            // carry into the next chunk: lane 31's run start if it is fluid
+            const int s31 = __shfl_sync(0xffffffffu, start, 31);
+            const bool f31 = __shfl_sync(0xffffffffu, fl ? 1 : 0, 31);
+            carry = f31 ? s31 : -1;
+        }
+    }
+}
+
+// y/z links between x-runs: only the first cell of each overlap segment
+// (where the -x neighbour pair is not already linked) unites.
+__global__ void k_uf_link_runs(const uint8_t *__restrict__ label, Dims d, int *par) {
+    int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
+    for (int64_t c = gtid(); c < nc; c += gstride()) {
+        if (label[c] != FLUID) continue;
+        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        const bool wfl = i > 0 && label[c - 1] == FLUID;
+        if (j > 0 && label[c - d.nx] == FLUID && !(wfl && label[c - 1 - d.nx] == FLUID))
+            uf_unite(par, (int)c, (int)(c - d.nx));
+        if (k > 0 && label[c - sxy] == FLUID && !(wfl && label[c - 1 - sxy] == FLUID))
+            uf_unite(par, (int)c, (int)(c - sxy));
+    }
+}
+
 __global__ void k_uf_link(const uint8_t *__restrict__ label, Dims d, int *par) {
     int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
     for (int64_t c = gtid(); c < nc; c += gstride()) {
@@ -1059,8 +1108,15 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     int64_t nc = c.ncells;
     cudaMemsetAsync(&c.sc->npinned, 0, sizeof(int), st);
     cudaMemsetAsync(&c.sc->rhsmax_bits, 0, sizeof(unsigned long long), st);
-    k_uf_init<<<nblocks(nc), kThreads, 0, st>>>(c.label, nc, c.parent, c.has_air);
-    k_uf_link<<<nblocks(nc), kThreads, 0, st>>>(c.label, c.d, c.parent);
+    static const bool uf_plain = getenv("FLIPB200_UF_PLAIN") != nullptr;
+    if (uf_plain) {
+        k_uf_init<<<nblocks(nc), kThreads, 0, st>>>(c.label, nc, c.parent, c.has_air);
+        k_uf_link<<<nblocks(nc), kThreads, 0, st>>>(c.label, c.d, c.parent);
+    } else {
+        const int64_t rows = (int64_t)c.d.ny * c.d.nz;
+        k_uf_runs<<<nblocks(rows * 32), kThreads, 0, st>>>(c.label, c.d, c.parent, c.has_air);
+        k_uf_link_runs<<<nblocks(nc), kThreads, 0, st>>>(c.label, c.d, c.parent);
+    }
     k_uf_finish<<<nblocks(nc), kThreads, 0, st>>>(c.label, c.d, c.parent, c.has_air);
     IsRowIn in{c.label, c.parent, c.has_air};
     exclusive_scan(in, nc, c.rowscan, &c.sc->nrows, c.scan_tmp, st);
