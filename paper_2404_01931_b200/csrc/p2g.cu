@@ -55,7 +55,7 @@ struct P2GOut {
 // from bin_particles).  !CONTIG: generic (offset, count) pairs per cell like
 // the Cython signature, used by the plugin API.
 template <bool CONTIG>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict__ py,
       const double *__restrict__ pz, const double *__restrict__ vel,
       const int *__restrict__ offset, const int *__restrict__ count, P2GOut out,
