@@ -199,6 +199,8 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     ALLOC(c->lvl_off, nlev + 1);
     ALLOC(c->lvl_cnt, nlev + 1);
     ALLOC(c->dot_part, dot_tmp_doubles(nc));
+    // the fused pairwise dot keeps a ticket word in this scratch: start at 0
+    FLIP_CUDA_OK(cudaMemset(c->dot_part, 0, sizeof(double) * dot_tmp_doubles(nc)));
     ALLOC(c->wave_prog, 8);
     ALLOC(c->wave_halo, wave_halo_doubles(nx, ny, nz));
     ALLOC(c->cflags, nc);
@@ -692,6 +694,7 @@ extern "C" int flip_energy_sums(flip_ctx *c, double floor_y, double *ke2, double
     k_energy_terms<<<nblocks(c->n), kThreads, 0, c->st>>>(c->P, c->n, floor_y, ke, pp);
     double *tmp = nullptr;
     FLIP_CUDA_OK(cudaMalloc(&tmp, sizeof(double) * dot_tmp_doubles(c->n)));
+    FLIP_CUDA_OK(cudaMemsetAsync(tmp, 0, sizeof(double) * dot_tmp_doubles(c->n), c->st));
     int64_t l = 0;
     launch_pairwise_dot(ke, nullptr, c->n, tmp, res, c->st, &l);
     launch_pairwise_dot(pp, nullptr, c->n, tmp, res + 1, c->st, &l);

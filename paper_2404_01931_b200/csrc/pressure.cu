@@ -398,6 +398,60 @@ __global__ void k_dot_tree(const double *__restrict__ in, int64_t cnt, double *_
     }
 }
 
+// k_dot_nodes + k_dot_tree in one launch when the node partials fit one tree
+// block (<= 1024): every block publishes its partial, the last block to
+// finish (threadfence + ticket) runs k_dot_tree's perfect-tree reduction and
+// the epilogue, then re-arms the ticket.  Same summation order.
+template <class LD>
+__global__ void k_dot_fused(LD ld, int64_t n, int cut, double *__restrict__ part,
+                            unsigned *ticket, int epi, DevScalars *sc, double *final_out,
+                            int skip_when_done) {
+    if (skip_when_done && sc->done) return;
+    __shared__ double sv[32];
+    __shared__ double sv2[1024];
+    __shared__ bool last;
+    int64_t nodes = (int64_t)1 << cut;
+    int64_t node = (int64_t)blockIdx.x * 32 + (threadIdx.x >> 3);
+    int g = threadIdx.x & 7;
+    double val = 0.0;
+    if (node < nodes) {
+        int64_t s0 = 0, len = n;
+        for (int lvl = cut - 1; lvl >= 0; lvl--) {
+            int64_t n2 = pw_split(len);
+            if ((node >> lvl) & 1) {
+                s0 += n2;
+                len -= n2;
+            } else {
+                len = n2;
+            }
+        }
+        val = pw_node8<2>(ld, s0, len, g);
+    }
+    if (g == 0) sv[threadIdx.x >> 3] = val;
+    __syncthreads();
+    int cnt = nodes < 32 ? (int)nodes : 32;
+    if (threadIdx.x == 0) {
+        for (int st = 1; st < cnt; st <<= 1)
+            for (int i = 0; i + st < cnt; i += 2 * st) sv[i] = sv[i] + sv[i + st];
+        part[blockIdx.x] = sv[0];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    const int m = (int)gridDim.x;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) sv2[i] = __ldcg(part + i);
+    __syncthreads();
+    for (int st = 1; st < m; st <<= 1) {
+        for (int i = threadIdx.x * 2 * st; i + st < m; i += blockDim.x * 2 * st) sv2[i] = sv2[i] + sv2[i + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        dot_epilogue(sv2[0], epi, final_out, sc);
+        *ticket = 0u;  // re-armed for the next dot
+    }
+}
+
 static int pw_cut(int64_t n) {
     // deepest depth at which all nodes exist (all shallower nodes split)
     std::vector<int64_t> sizes{n};
@@ -436,6 +490,14 @@ static void launch_dot_f(const LD &ld, int64_t n, double *tmp, double *out_dev, 
     double *p0 = tmp, *p1 = tmp + nb1;
     // only the solver's in-loop dots may skip their work after convergence
     const bool skip = epi == EPI_CURV || epi == EPI_SIGMA_NEW;
+    if (nb1 <= 1024) {
+        // ticket: the word after the partials (zeroed at allocation, re-armed by the kernel)
+        unsigned *ticket = reinterpret_cast<unsigned *>(tmp + 2 * nb1);
+        k_dot_fused<LD><<<(unsigned)nb1, 256, 0, st>>>(ld, n, cut, p0, ticket, epi, sc, out_dev,
+                                                       skip ? 1 : 0);
+        (*launches)++;
+        return;
+    }
     k_dot_nodes<LD><<<(unsigned)nb1, 256, 0, st>>>(ld, n, cut, p0, skip ? sc : nullptr);
     (*launches)++;
     int64_t cnt = nb1;
@@ -1247,6 +1309,8 @@ struct DevArena {
     T *get(int64_t n) {
         void *p = nullptr;
         if (cudaMalloc(&p, sizeof(T) * (size_t)(n > 0 ? n : 1)) != cudaSuccess) return nullptr;
+        // zeroed: dot scratch carries the fused dot's ticket word
+        cudaMemset(p, 0, sizeof(T) * (size_t)(n > 0 ? n : 1));
         ptrs.push_back(p);
         return (T *)p;
     }
