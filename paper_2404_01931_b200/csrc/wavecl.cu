@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
     constexpr int DY = TY - 1, DZ = TZ - 1;
     __shared__ double sval[2][TZ + 2][TY + 2];
     __shared__ int s_tile;
-    __shared__ __align__(8) unsigned long long mbar[NB];
+    __shared__ __align__(8) unsigned long long mbar[NB > 0 ? NB : 1];
     // yring[nsteps][TZ], zring[nsteps][TY], then the operand chunks
     extern __shared__ __align__(128) double ring[];
     const int t = threadIdx.x;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
         const int64_t tbase = (int64_t)tile * nsteps * TP;
         const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
         const int lo = REV ? nsteps - s0 - cnt : s0;
-        const int buf = ch % NB;
+        const int buf = ch % (NB > 0 ? NB : 1);
         const unsigned bytes = (unsigned)(cnt * TP * 8);
         mbar_expect_tx(&mbar[buf], 2 * bytes);
         bulk_g2s(opb + (buf * 2 + 0) * KC * TP, A.src + tbase + (int64_t)lo * TP, bytes, &mbar[buf]);
@@ -163,35 +163,28 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
         const int kk = yface ? l : 0, jj = zface ? l - TZ : 0;
         const int W = yface ? TZ : TY;
         const int D = yface ? DY : DZ;
-        const double *in = nullptr;
-        double *out = nullptr;
-        int in_row = 0, in_col = 0, out_row = 0, out_col = 0, cons_j = 0, cons_k = 0;
+        const double *in = nullptr;  // producing lanes publish their own faces
+        int in_row = 0, in_col = 0, cons_j = 0, cons_k = 0;
         if (yface) {
             cons_j = REV ? TY - 1 : 0;
             cons_k = kk;
             const bool has = REV ? b + 1 < G.TB : b > 0;
             if (has && !ydin)
                 in = A.halo_y + (int64_t)(REV ? tile + G.TC : tile - G.TC) * nsteps * TZ + kk;
-            if (!ydout && (A.mode & 1)) out = A.halo_y + (int64_t)tile * nsteps * TZ + kk;
             in_row = kk + 1;
             in_col = REV ? TY + 1 : 0;
-            out_row = kk + 1;
-            out_col = (REV ? 0 : TY - 1) + 1;
         } else if (zface) {
             cons_j = jj;
             cons_k = REV ? TZ - 1 : 0;
             const bool has = REV ? c + 1 < G.TC : c > 0;
             if (has && !zdin)
                 in = A.halo_z + (int64_t)(REV ? tile + 1 : tile - 1) * nsteps * TY + jj;
-            if (!zdout && (A.mode & 1)) out = A.halo_z + (int64_t)tile * nsteps * TY + jj;
             in_row = REV ? TZ + 1 : 0;
             in_col = jj + 1;
-            out_row = (REV ? 0 : TZ - 1) + 1;
-            out_col = jj + 1;
         }
         const bool cvalid = G.jlo + b * TY + cons_j <= G.jhi && G.klo + c * TZ + cons_k <= G.khi;
         if (!cvalid) in = nullptr;
-        if (l == 0)
+        if (NB > 0 && l == 0)
             for (int q = 0; q < NB; q++) issue(q);
         double hr[UH];
         auto fetch = [&](int s, int u) {
@@ -207,13 +200,12 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 const int s = s0 + u;
                 if (s >= nsteps) break;
                 __syncthreads();
-                if (l == 0 && s > 0 && s % KC == 0) {
+                if (NB > 0 && l == 0 && s > 0 && s % KC == 0) {
                     // every compute thread finished chunk s/KC - 1 before this barrier
                     fence_proxy_async();
                     issue(s / KC - 1 + NB);
                 }
                 const int cur = s & 1, prv = cur ^ 1;
-                if (out && s > 0) publish(out + (int64_t)(s - 1) * W, sval[prv][out_row][out_col]);
                 if (in) {
                     double v = hr[u];
                     if (is_pending(v)) v = poll_ready(in + (int64_t)(s + 1 + D) * W);
@@ -223,7 +215,6 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
             }
         }
         __syncthreads();
-        if (out) publish(out + (int64_t)(nsteps - 1) * W, sval[(nsteps - 1) & 1][out_row][out_col]);
     } else {
         // ------------------------------------------------- compute warps
         const int jj = t % TY, kk = t / TY;
@@ -237,19 +228,67 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
         const unsigned zout = (zdout && kk == prod_k) ? map_rank(zring + jj, cr + 1) : 0u;
         // faces leaving the cluster: the producing lanes publish to the global
         // halo themselves (one store per step, no helper round trip)
-        double *gy = (!ydout && jj == prod_j && !(A.mode & 1))
+        double *gy = (!ydout && jj == prod_j)
                          ? A.halo_y + (int64_t)tile * nsteps * TZ + kk : nullptr;
-        double *gz = (!zdout && kk == prod_k && !(A.mode & 1))
+        double *gz = (!zdout && kk == prod_k)
                          ? A.halo_z + (int64_t)tile * nsteps * TY + jj : nullptr;
         const int yr = kk + 1, yc = REV ? jj + 2 : jj, zr = REV ? kk + 2 : kk, zc = jj + 1;
         const int64_t base = (int64_t)tile * nsteps * TP + t;
         double *dstL = A.dst + base;
         double pv = nz0;
         const double sc = A.scale;
-        for (int ch = 0; ch < nch; ch++) {
+        if constexpr (NB == 0) {
+            // operands straight into registers KC steps ahead (coalesced 8-byte
+            // loads from the lane-major layout), no shared-memory round trip
+            const int64_t base = (int64_t)tile * nsteps * TP + t;
+            const double *srcL = A.src + base, *preL = A.precon + base;
+            double av[KC], bv[KC];
+            auto load = [&](int s, int u) {
+                const int sl = max(min(lstep(s), nsteps - 1), 0);
+                av[u] = __ldcs(srcL + (int64_t)sl * TP);
+                bv[u] = __ldcs(preL + (int64_t)sl * TP);
+            };
+#pragma unroll
+            for (int u = 0; u < KC; u++) load(u, u);
+            for (int s0 = 0; s0 < nsteps; s0 += KC) {
+#pragma unroll
+                for (int u = 0; u < KC; u++) {
+                    const int s = s0 + u;
+                    if (s >= nsteps) break;
+                    __syncthreads();
+                    const int cur = s & 1, prv = cur ^ 1;
+                    const double a = av[u], pr = bv[u];
+                    load(s + KC, u);
+                    double yv = sval[prv][yr][yc], zv = sval[prv][zr][zc];
+                    if (yin) yv = s + DY < nsteps ? poll_local(yring + (s + DY) * TZ + kk) : nz0;
+                    if (zin) zv = s + DZ < nsteps ? poll_local(zring + (s + DZ) * TY + jj) : nz0;
+                    const bool row = valid && present(a);
+                    double o;
+                    if (!REV) {  // _core.pyx:322-332
+                        double tt = ((a + pv) + yv) + zv;
+                        double q = tt * pr;
+                        if (row) dstL[(int64_t)lstep(s) * TP] = q;
+                        o = (sc * pr) * q;
+                    } else {     // _core.pyx:333-346
+                        double sp = sc * pr;
+                        double tt = ((a + sp * pv) + sp * yv) + sp * zv;
+                        o = tt * pr;
+                        if (row) dstL[(int64_t)lstep(s) * TP] = o;
+                    }
+                    o = row ? o : nz0;
+                    sval[cur][kk + 1][jj + 1] = o;
+                    pv = o;
+                    if (yout) st_remote(yout + (unsigned)(s * TZ * 8), o);
+                    if (zout) st_remote(zout + (unsigned)(s * TY * 8), o);
+                    if (gy) publish(gy + (int64_t)s * TZ, o);
+                    if (gz) publish(gz + (int64_t)s * TY, o);
+                }
+            }
+        }
+        for (int ch = 0; NB > 0 && ch < nch; ch++) {
             const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
-            const int buf = ch % NB;
-            if (!(A.mode & 128)) mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
+            const int buf = ch % (NB > 0 ? NB : 1);
+            mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
             const double *ab = opb + (buf * 2 + 0) * KC * TP + t;
             const double *pb = opb + (buf * 2 + 1) * KC * TP + t;
 #pragma unroll
@@ -259,11 +298,10 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 __syncthreads();
                 const int cur = s & 1, prv = cur ^ 1;
                 const int idx = REV ? cnt - 1 - u : u;
-                const double a = (A.mode & 128) ? 1.0 : ab[idx * TP];
-                const double pr = (A.mode & 128) ? 0.5 : pb[idx * TP];
+                const double a = ab[idx * TP], pr = pb[idx * TP];
                 double yv = sval[prv][yr][yc], zv = sval[prv][zr][zc];
-                if (yin && !(A.mode & 64)) yv = s + DY < nsteps ? poll_local(yring + (s + DY) * TZ + kk) : nz0;
-                if (zin && !(A.mode & 64)) zv = s + DZ < nsteps ? poll_local(zring + (s + DZ) * TY + jj) : nz0;
+                if (yin) yv = s + DY < nsteps ? poll_local(yring + (s + DY) * TZ + kk) : nz0;
+                if (zin) zv = s + DZ < nsteps ? poll_local(zring + (s + DZ) * TY + jj) : nz0;
                 if (A.trace && !REV && t == 0 && tile < 8 && s < 300) {
                     unsigned long long g;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
@@ -274,7 +312,7 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 if (!REV) {  // _core.pyx:322-332
                     double tt = ((a + pv) + yv) + zv;
                     double q = tt * pr;
-                    if (row && !(A.mode & 16)) dstL[(int64_t)lstep(s) * TP] = q;
+                    if (row) dstL[(int64_t)lstep(s) * TP] = q;
                     o = (sc * pr) * q;
                 } else {     // _core.pyx:333-346
                     double sp = sc * pr;
@@ -285,12 +323,10 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 o = row ? o : nz0;
                 sval[cur][kk + 1][jj + 1] = o;
                 pv = o;
-                if (!(A.mode & 32)) {
-                    if (yout) st_remote(yout + (unsigned)(s * TZ * 8), o);
-                    if (zout) st_remote(zout + (unsigned)(s * TY * 8), o);
-                    if (gy) publish(gy + (int64_t)s * TZ, o);
-                    if (gz) publish(gz + (int64_t)s * TY, o);
-                }
+                if (yout) st_remote(yout + (unsigned)(s * TZ * 8), o);
+                if (zout) st_remote(zout + (unsigned)(s * TY * 8), o);
+                if (gy) publish(gy + (int64_t)s * TZ, o);
+                if (gz) publish(gz + (int64_t)s * TY, o);
             }
         }
         __syncthreads();  // matches the helper's final barrier
@@ -331,8 +367,9 @@ int mic_cluster_pad(int *cy, int *cz) { return cluster_shape(cy, cz); }
 // operand chunk ring: KC steps per bulk copy, NB chunks in flight, and an
 // optional L2 prefetch L2AHEAD chunks further (FLIPB200_CL_CHUNKS=KCxNB[xL2]).
 // Measured at 256^3 (project stage, 4x4 clusters): 4x3 65.8 ms, 4x8 69.8,
-// 8x4 67.7, 4x3 + L2 prefetch 4 or 6 chunks ahead 65.8-65.9: deeper smem
-// rings cost residency, and operand latency is not what bounds the loop.
+// 8x4 67.7, 4x3 + L2 prefetch 4 or 6 chunks ahead 65.8-65.9, "8x0" (no
+// ring: operands loaded into registers 8 steps ahead) 87.4: deeper smem
+// rings cost residency, registers expose the memory latency.
 static int chunk_cfg() {
     static int v = -1;
     if (v < 0) {
@@ -384,6 +421,7 @@ static cudaError_t launch_cl(const LaneArgs &A, cudaStream_t st) {
         case 408: return launch_cl_k<REV, CY, CZ, 4, 8, 0>(A, st);
         case 4036: return launch_cl_k<REV, CY, CZ, 4, 3, 6>(A, st);
         case 4034: return launch_cl_k<REV, CY, CZ, 4, 3, 4>(A, st);
+        case 800: return launch_cl_k<REV, CY, CZ, 8, 0, 0>(A, st);
         default: return launch_cl_k<REV, CY, CZ, 4, 3, 0>(A, st);
     }
 }

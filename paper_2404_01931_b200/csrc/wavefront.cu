@@ -821,141 +821,6 @@ __global__ void __launch_bounds__(TY *TZ + 32) k_mic_lane2(LaneArgs A) {
     }
 }
 
-// k_mic_lane3 (FLIPB200_LANE_V3, experimental; measured slower than
-// k_mic_lane2 at 256^3: 94 vs 72 ms per PCG solve): k_mic_lane2 without the helper warp.  Face lanes publish their
-// own outputs (one 8-byte store per step) and keep their own register ring of
-// incoming face values, so a step is barrier -> body -> barrier with nothing
-// serialised behind the compute.  Same halo layout (step-major), same
-// arithmetic, same bulk-copy operand staging.
-template <bool REV, int TY, int TZ, int U, int KC>
-__global__ void __launch_bounds__(TY *TZ) k_mic_lane3(LaneArgs A) {
-    constexpr int TP = TY * TZ;
-    __shared__ double sval[2][TZ + 2][TY + 2];
-    __shared__ int s_tile;
-    __shared__ __align__(8) unsigned long long mbar[LANE_NB];
-    extern __shared__ __align__(128) double opb[];
-    const int t = threadIdx.x;
-    if (A.sc && A.sc->done) return;
-    const WaveGeom G = A.geom;
-    if (t == 0) s_tile = atomicAdd(A.ticket, 1);
-    const double nz0 = -0.0;
-    for (int q = t; q < 2 * (TZ + 2) * (TY + 2); q += blockDim.x) (&sval[0][0][0])[q] = nz0;
-    __syncthreads();
-    int b, c;
-    ticket_tile(s_tile, G.TB, G.TC, b, c);
-    if (REV) {
-        b = G.TB - 1 - b;
-        c = G.TC - 1 - c;
-    }
-    const int tile = b * G.TC + c;
-    const int nsteps = G.nsteps;
-    auto lstep = [&](int s) { return REV ? nsteps - 1 - s : s; };
-    const int jj = t % TY, kk = t / TY;
-    const bool valid = G.jlo + b * TY + jj <= G.jhi && G.klo + c * TZ + kk <= G.khi;
-
-    // faces: consumer lanes read a ring of predecessor values, producer lanes publish
-    const int cons_j = REV ? TY - 1 : 0, cons_k = REV ? TZ - 1 : 0;
-    const int prod_j = REV ? 0 : TY - 1, prod_k = REV ? 0 : TZ - 1;
-    const bool ypred = REV ? b + 1 < G.TB : b > 0;
-    const bool zpred = REV ? c + 1 < G.TC : c > 0;
-    const double *yin = (valid && jj == cons_j && ypred)
-                            ? A.halo_y + (int64_t)(REV ? tile + G.TC : tile - G.TC) * nsteps * TZ + kk
-                            : nullptr;
-    const double *zin = (valid && kk == cons_k && zpred)
-                            ? A.halo_z + (int64_t)(REV ? tile + 1 : tile - 1) * nsteps * TY + jj
-                            : nullptr;
-    double *yout = jj == prod_j ? A.halo_y + (int64_t)tile * nsteps * TZ + kk : nullptr;
-    double *zout = kk == prod_k ? A.halo_z + (int64_t)tile * nsteps * TY + jj : nullptr;
-    // consumer at step s needs the producer's step s + D
-    constexpr int DY = TY - 1, DZ = TZ - 1;
-    double ry[U], rz[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-        ry[u] = (yin && u + DY < nsteps) ? ld_relaxed(yin + (int64_t)(u + DY) * TZ) : nz0;
-        rz[u] = (zin && u + DZ < nsteps) ? ld_relaxed(zin + (int64_t)(u + DZ) * TY) : nz0;
-    }
-
-    const int yr = kk + 1, yc = REV ? jj + 2 : jj, zr = REV ? kk + 2 : kk, zc = jj + 1;
-    const int64_t base = (int64_t)tile * nsteps * TP + t;
-    double *dstL = A.dst + base;
-    double pv = nz0;
-    const double sc = A.scale;
-
-    const int nch = (nsteps + KC - 1) / KC;
-    const int64_t tbase = (int64_t)tile * nsteps * TP;
-    auto issue = [&](int ch) {  // thread 0 only
-        if (ch >= nch) return;
-        const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
-        const int lo = REV ? nsteps - s0 - cnt : s0;
-        const int buf = ch % LANE_NB;
-        const unsigned bytes = (unsigned)(cnt * TP * 8);
-        mbar_expect_tx(&mbar[buf], 2 * bytes);
-        bulk_g2s(opb + (buf * 2 + 0) * KC * TP, A.src + tbase + (int64_t)lo * TP, bytes, &mbar[buf]);
-        bulk_g2s(opb + (buf * 2 + 1) * KC * TP, A.precon + tbase + (int64_t)lo * TP, bytes,
-                 &mbar[buf]);
-    };
-    if (t == 0) {
-        for (int q = 0; q < LANE_NB; q++) mbar_init(&mbar[q], 1);
-        mbar_fence_init();
-        for (int q = 0; q < LANE_NB; q++) issue(q);
-    }
-    __syncthreads();  // mbarrier init visible
-    for (int ch = 0; ch < nch; ch++) {
-        const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
-        const int buf = ch % LANE_NB;
-        mbar_wait(&mbar[buf], (unsigned)(ch / LANE_NB) & 1u);
-        const double *ab = opb + (buf * 2 + 0) * KC * TP + t;
-        const double *pb = opb + (buf * 2 + 1) * KC * TP + t;
-#pragma unroll
-        for (int u = 0; u < KC; u++) {
-            if (u >= cnt) break;
-            const int s = s0 + u;
-            const int ru = u % U;  // KC is a multiple of U
-            if (u > 0 || ch > 0) __syncthreads();
-            if (u == 0 && ch > 0 && t == 0) {
-                fence_proxy_async();
-                issue(ch - 1 + LANE_NB);
-            }
-            const int idx = REV ? cnt - 1 - u : u;
-            const double a = ab[idx * TP], pr = pb[idx * TP];
-            const int cur = s & 1, prv = cur ^ 1;
-            double yv = sval[prv][yr][yc], zv = sval[prv][zr][zc];
-            if (yin) {
-                double v = ry[ru];
-                if (s + DY < nsteps && is_pending(v)) v = poll_ready(yin + (int64_t)(s + DY) * TZ);
-                yv = v;
-                const int sn = s + U + DY;
-                ry[ru] = sn < nsteps ? ld_relaxed(yin + (int64_t)sn * TZ) : nz0;
-            }
-            if (zin) {
-                double v = rz[ru];
-                if (s + DZ < nsteps && is_pending(v)) v = poll_ready(zin + (int64_t)(s + DZ) * TY);
-                zv = v;
-                const int sn = s + U + DZ;
-                rz[ru] = sn < nsteps ? ld_relaxed(zin + (int64_t)sn * TY) : nz0;
-            }
-            const bool row = valid && present(a);
-            double o;
-            if (!REV) {  // _core.pyx:322-332 (absent terms are -0.0: exact no-ops)
-                double tt = ((a + pv) + yv) + zv;
-                double q = tt * pr;
-                if (row) dstL[(int64_t)lstep(s) * TP] = q;
-                o = (sc * pr) * q;
-            } else {     // _core.pyx:333-346
-                double sp = sc * pr;
-                double tt = ((a + sp * pv) + sp * yv) + sp * zv;
-                o = tt * pr;
-                if (row) dstL[(int64_t)lstep(s) * TP] = o;
-            }
-            o = row ? o : nz0;
-            sval[cur][kk + 1][jj + 1] = o;
-            pv = o;
-            if (yout) publish(yout + (int64_t)s * TZ, o);
-            if (zout) publish(zout + (int64_t)s * TY, o);
-        }
-    }
-}
-
 // L-layout maps: lrow[e] = row at entry e (or -1); posL[row] = e.
 __global__ void k_lane_map(WaveGeom G, Dims d, int TY, int TZ, const uint8_t *__restrict__ isrow,
                            const int *__restrict__ rowscan, int *__restrict__ lrow,
@@ -1153,18 +1018,7 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
             cudaError_t e = launch_mic_cluster(REV, B, st);
             if (e != cudaErrorNotSupported) return e;
         }
-        static const bool v3 = getenv("FLIPB200_LANE_V3") != nullptr;
-        if (v3) {
-            constexpr int KC = 8;
-            constexpr int smem = LANE_NB * 2 * KC * TY * TZ * 8;
-            static bool attr3 = [] {
-                cudaFuncSetAttribute(k_mic_lane3<REV, TY, TZ, 4, KC>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                return true;
-            }();
-            (void)attr3;
-            k_mic_lane3<REV, TY, TZ, 4, KC><<<(unsigned)tiles, TY * TZ, smem, st>>>(B);
-        } else if (lane_chunk() > 0) {
+        if (lane_chunk() > 0) {
             constexpr int KC = 8;
             constexpr int smem = LANE_NB * 2 * KC * TY * TZ * 8;
             static bool attr = [] {
