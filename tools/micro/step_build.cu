@@ -19,17 +19,18 @@ __device__ __forceinline__ void bulk(void *d, const void *s, unsigned n, unsigne
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa(d)), "l"(s), "r"(n), "r"(sa(b)) : "memory");
 }
 
-template <int OPS, int HLP, int MB, int RMT, int NB = 2>
+template <int OPS, int HLP, int MB, int RMT, int NB = 2, int CONS = 0, int PF = 0>
 __global__ void __launch_bounds__(288) k(int steps, const double *src, double *dst, unsigned long long *cyc) {
     constexpr int KC = 4, TP = 256;
     __shared__ double sval[2][18][18];
     extern __shared__ __align__(128) double opb_raw[];
     auto opb = reinterpret_cast<double (*)[2][KC][TP]>(opb_raw);
     __shared__ __align__(8) unsigned long long mbar[NB];
-    __shared__ __align__(16) double peer_ring[64][16];
+    __shared__ __align__(16) double peer_ring[256][16];  // whole run: slots never reused
     const int t = threadIdx.x;
     for (int q = t; q < 2 * 18 * 18; q += blockDim.x) (&sval[0][0][0])[q] = 0.0;
     for (int q = t; q < NB * 2 * KC * TP; q += blockDim.x) (&opb[0][0][0][0])[q] = 1.0;
+    for (int q = t; q < 256 * 16; q += blockDim.x) (&peer_ring[0][0])[q] = CONS ? __longlong_as_double(0x7ff8dead00000001LL) : 0.0;
     if (t == 0) { for (int q = 0; q < NB; q++) mb_init(&mbar[q]); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
     asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
     unsigned rk; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rk));
@@ -58,6 +59,8 @@ __global__ void __launch_bounds__(288) k(int steps, const double *src, double *d
     if (MB && !HLP && t == 0) for (int q = 0; q < NB; q++) issue(q);
     const int jj = t & 15, kk = t >> 4;
     double pv = 0.0, sc = 0.25;
+    volatile double *peer_ring_v = &peer_ring[0][0];
+    double znext = CONS ? peer_ring_v[0 * 16 + (t & 15)] : 0.0;
     double *d = dst + (size_t)blockIdx.x * steps * TP + t;
     long long c0 = clock64();
     for (int s = 0; s < steps; s++) {
@@ -70,24 +73,33 @@ __global__ void __launch_bounds__(288) k(int steps, const double *src, double *d
         }
         const int cur = s & 1, prv = cur ^ 1;
         double a = 1e-3 * t, pr = 0.5;
+        double zin = 0.0;
+        if (CONS && rk == 1 && kk == 0 && s >= 16) {  // consume rank 0's output of step s-16
+            volatile double *slot = &peer_ring[(s - 16) & 255][jj];
+            double v = PF ? znext : *slot;
+            while (v != v) v = *slot;  // NaN = not yet written
+            zin = v;
+            if (PF) znext = peer_ring_v[((s - 15) & 255) * 16 + jj];  // next step's value, early
+        }
         if (OPS) { a = opb[ch % NB][0][u][t]; pr = opb[ch % NB][1][u][t]; }
         double yv = sval[prv][kk + 1][jj], zv = sval[prv][kk][jj + 1];
-        double tt = ((a + pv) + yv) + zv;
+        double tt = ((a + pv) + yv) + (zv + zin);
         double q = tt * pr;
         if (OPS && a != 12345.0) d[(size_t)s * TP] = q;
         double o = (sc * pr) * q;
         sval[cur][kk + 1][jj + 1] = o;
         pv = o;
-        if (RMT && kk == 15)
-            asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(peer + (unsigned)(((s & 63) * 16 + jj) * 8)), "d"(o) : "memory");
+        if (RMT && kk == 15 && (!CONS || rk == 0))
+            asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(peer + (unsigned)(((s & 255) * 16 + jj) * 8)), "d"(o) : "memory");
     }
     long long c1 = clock64();
     if (t == 0 && blockIdx.x == 0) cyc[0] = (c1 - c0) / steps;
+    if (t == 0 && blockIdx.x == 1) cyc[1] = (c1 - c0) / steps;
     asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
     (void)nthr;
 }
 
-template <int OPS, int HLP, int MB, int RMT, int NB = 2>
+template <int OPS, int HLP, int MB, int RMT, int NB = 2, int CONS = 0, int PF = 0>
 void run(const char *name, const double *src, double *dst, unsigned long long *cyc, int steps) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(296);
@@ -97,17 +109,17 @@ void run(const char *name, const double *src, double *dst, unsigned long long *c
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at; cfg.numAttrs = 1;
     cfg.dynamicSmemBytes = NB * 2 * 4 * 256 * 8;
-    cudaFuncSetAttribute(k<OPS, HLP, MB, RMT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k<OPS, HLP, MB, RMT, NB, CONS, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, NB * 2 * 4 * 256 * 8);
     for (int rep = 0; rep < 2; rep++) {
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k<OPS, HLP, MB, RMT, NB>, steps, src, dst, cyc);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k<OPS, HLP, MB, RMT, NB, CONS, PF>, steps, src, dst, cyc);
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("%s: err %s\n", name, cudaGetErrorString(e)); return; }
     }
-    printf("%-34s %llu cycles/step\n", name, cyc[0]);
+    printf("%-44s %llu cycles/step (rank1 %llu)\n", name, cyc[0], cyc[1]);
 }
 
 int main() {
-    const int steps = 512;
+    const int steps = 256;
     double *src, *dst;
     unsigned long long *cyc;
     size_t n = (size_t)296 * steps * 256;
@@ -123,6 +135,10 @@ int main() {
     run<1, 0, 1, 0>("+ops +mbar (thread 0 issues)", src, dst, cyc, steps);
     run<1, 1, 1, 0, 4>("+ops +helper +mbar NB=4", src, dst, cyc, steps);
     run<1, 1, 1, 0, 8>("+ops +helper +mbar NB=8", src, dst, cyc, steps);
-    run<1, 1, 1, 0, 16>("+ops +helper +mbar NB=16", src, dst, cyc, steps);
+    run<1, 1, 1, 1, 8>("+ops +helper +mbar NB=8 +remote", src, dst, cyc, steps);
+    run<1, 1, 1, 1, 8, 1>("+ops +helper +mbar NB=8 +remote +consumer", src, dst, cyc, steps);
+    run<0, 1, 0, 1, 2, 1>("skeleton +helper +remote +consumer", src, dst, cyc, steps);
+    run<1, 1, 1, 1, 8, 1, 1>("+ops +helper +mbar NB=8 +remote +consumer PF", src, dst, cyc, steps);
+    run<0, 1, 0, 1, 2, 1, 1>("skeleton +helper +remote +consumer PF", src, dst, cyc, steps);
     return 0;
 }
