@@ -57,13 +57,20 @@ def parse():
     ap.add_argument("--res", type=int, default=256)
     ap.add_argument("--scene", default="dam-break")
     ap.add_argument("--solver", default="pcg")
+    ap.add_argument("--precond", default="mic0",
+                    help="mic0 (the reference's, default) or mg (extension: multigrid, "
+                         "converged, tolerance-validated)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
 def workload(args) -> dict:
-    prec = "MIC(0)-PCG, cap 100" if args.solver == "pcg" else f"{args.solver}, cap 2000"
+    if args.solver == "pcg":
+        prec = ("MIC(0)-PCG, cap 100" if getattr(args, "precond", "mic0") == "mic0"
+                else f"{args.precond}-PCG (extension), cap 100")
+    else:
+        prec = f"{args.solver}, cap 2000"
     return {"workload": f"{args.scene} {args.res}^3, density 2 (8 particles/cell), {prec}, "
                         f"tol 1e-6, flip 0.95, seed 0",
             "res": args.res, "scene": args.scene, "solver": args.solver,
@@ -205,7 +212,7 @@ def run_ours(args):
     from paper_2404_01931_b200 import _lib
     from paper_2404_01931_b200._lib import LIB, check
 
-    spec = P.SceneSpec(name=args.scene, res=args.res, solver=args.solver)
+    spec = P.SceneSpec(name=args.scene, res=args.res, solver=args.solver, precond=args.precond)
     if world > 1:
         from paper_2404_01931_b200 import dist as D
         st = D.make_scene(spec, rng_seed=0, device=local)

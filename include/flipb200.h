@@ -67,6 +67,9 @@ extern "C" {
 #define FLIP_PRECOND_MIC0 0
 #define FLIP_PRECOND_JACOBI 1
 #define FLIP_PRECOND_NONE 2
+/* extension: geometric multigrid V-cycle; results differ from
+ * the reference (which has only MIC(0)) and are validated to tolerance */
+#define FLIP_PRECOND_MG 3
 
 typedef struct flip_ctx flip_ctx;
 

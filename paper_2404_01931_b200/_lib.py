@@ -27,7 +27,7 @@ NSTAGES = len(STAGE_NAMES)
 STAGE = {name: i for i, name in enumerate(STAGE_NAMES)}
 
 SOLVER_ID = {"jacobi": 0, "gs": 1, "rbgs": 2, "pcg": 3}
-PRECOND_ID = {"mic0": 0, "jacobi": 1, "none": 2}
+PRECOND_ID = {"mic0": 0, "jacobi": 1, "none": 2, "mg": 3}
 
 
 class StepParams(C.Structure):

@@ -95,6 +95,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->st) cudaStreamSynchronize(c->st);
+    mg_free(*c);
     void *ptrs[] = {c->P.a[0], c->P.a[1], c->P.a[2], c->P.a[3], c->P.a[4], c->P.a[5], c->Q.a[0],
                     c->Q.a[1], c->Q.a[2], c->Q.a[3], c->Q.a[4], c->Q.a[5], c->u, c->v, c->w, c->p,
                     c->label, c->uo, c->vo, c->wo, c->ku, c->kv, c->kw, c->ku1, c->kv1, c->kw1,
@@ -540,7 +541,7 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
         set_error("bad stage range");
         return FLIP_E_ARG;
     }
-    if (prm->solver < 0 || prm->solver > 3 || prm->precond < 0 || prm->precond > 2) {
+    if (prm->solver < 0 || prm->solver > 3 || prm->precond < 0 || prm->precond > FLIP_PRECOND_MG) {
         set_error("unknown solver or preconditioner");
         return FLIP_E_CONFIG;
     }

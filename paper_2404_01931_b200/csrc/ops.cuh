@@ -51,6 +51,7 @@ struct Ctx {
     int64_t n = 0;          // particle count (host mirror)
     int64_t slab_c0 = 0, slab_c1 = -1;  // reseed cell range (flip_set_slab); -1: all
     void *f32_buf = nullptr;           // snapshot staging (flip_*_particles_f32)
+    void *mg = nullptr;                // multigrid levels (mg.cu), allocated on first use
     size_t f32_cap = 0;
     ParticlePtrs P{}, Q{};  // current and back particle buffers
     double *u = nullptr, *v = nullptr, *w = nullptr, *p = nullptr;
@@ -119,6 +120,11 @@ void stage_reseed(Ctx &c, const flip_step_params &prm);
 void launch_particle_cells(Ctx &c, int *out);
 void launch_set_solid_box(Ctx &c, const int b[6]);
 void launch_particles_f32(Ctx &c, float *buf, bool to_f32);
+// mg.cu: multigrid preconditioner (precond = FLIP_PRECOND_MG)
+int mg_setup(Ctx &c, double scale, const int lo[3], const int hi[3], cudaStream_t st);
+void mg_apply(Ctx &c, const double *r, double *z, int64_t n, const DevScalars *sc,
+              cudaStream_t st, int64_t *launches);
+void mg_free(Ctx &c);
 
 void launch_set_solid_shell(Ctx &c);
 int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed);

@@ -966,6 +966,7 @@ struct SweepLevels {
     const WaveArgs *wave;  // non-null: use the pipelined wavefront
     Probe *probe;          // optional event bracketing of the MIC substitutions
     const LaneBufs *lane;  // non-null: MIC(0) apply through the lane-major kernels
+    Ctx *mg = nullptr;     // multigrid preconditioner state (FLIP_PRECOND_MG)
 };
 
 template <int MODE>
@@ -1007,6 +1008,10 @@ static cudaError_t g_sweep_launch_err = cudaSuccess;
 static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                      const SweepLevels &LV, const double *r, double *z, DevScalars *sc,
                      cudaStream_t st, int64_t *launches, bool fused = false) {
+    if (cfg.precond == FLIP_PRECOND_MG) {
+        mg_apply(*LV.mg, r, z, S.n, sc, st, launches);
+        return;
+    }
     if (cfg.precond == FLIP_PRECOND_MIC0 && LV.lane) {
         // r -> L layout, forward (L), backward (L), back to rows
         const LaneBufs &Lb = *LV.lane;
@@ -1253,7 +1258,9 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         launch_lane_map(W.geom, c.d, c.isrow, c.rowscan, c.lrow, c.posL, c.laneA, c.laneB, st);
         c.launches++;
     }
-    SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr, &c.probe, use_lane ? &LB : nullptr};
+    SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr, &c.probe, use_lane ? &LB : nullptr, &c};
+    if (prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MG && n > 0)
+        if (int rc = mg_setup(c, scale, c.sch->row_lo, c.sch->row_hi, st)) return rc;
     SolveCfg cfg{prm.solver, prm.precond, prm.max_iters, prm.tol, prm.solver_check_every, nullptr,
                  nullptr, nullptr, 0, 0, c.d};
     SolveBufs B{c.x, c.r, c.z, c.s, c.q, c.tq, c.precon, c.xtmp, c.dot_part, c.scan_tmp,
@@ -1537,7 +1544,7 @@ extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, con
                                  int64_t nblack, double *x, int64_t *iterations, double *residual,
                                  int32_t *converged, int64_t *err_cell, int64_t *err_iteration,
                                  double *err_value) {
-    if (solver < 0 || solver > 3 || precond < 0 || precond > 2) {
+    if (solver < 0 || solver > 3 || precond < 0 || precond > FLIP_PRECOND_MG) {
         set_error("unknown solver or preconditioner");
         return FLIP_E_CONFIG;
     }
@@ -1573,6 +1580,10 @@ extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, con
     SysView V{n, c32, nb, n, dd, dr, scale};
     int *scan_tmp = ar.get<int>(scan_tmp_ints(n + 2) + 8);
     Levels Lf{}, Lb{}, Lg{};
+    if (precond == FLIP_PRECOND_MG) {
+        set_error("the multigrid preconditioner needs the grid (use it through flip_step)");
+        return FLIP_E_ARG;
+    }
     bool mic = solver == FLIP_SOLVER_PCG && precond == FLIP_PRECOND_MIC0;
     if (n > 0 && mic) {
         if (int rc = generic_levels(ar, V, 0, Lf, S.st, scan_tmp)) return rc;

@@ -24,7 +24,7 @@ from .particles import ParticleSet, SeedRegion, covered_cells
 
 SCENE_NAMES = ("dam-break", "double-dam-break", "water-drop", "double-dam-break-obstacle")
 SOLVERS = ("jacobi", "gs", "rbgs", "pcg")
-PRECONDITIONERS = ("mic0", "jacobi", "none")
+PRECONDITIONERS = ("mic0", "jacobi", "none", "mg")   # "mg": extension, tolerance-validated
 
 
 @dataclass
