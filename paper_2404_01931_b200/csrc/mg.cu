@@ -198,6 +198,39 @@ __global__ void k_mg_gather(const double *__restrict__ x0, const int *__restrict
         zrows[r] = x0[mg_region(d, ox, oy, oz, nx, ny, cell_of_row[r])];
 }
 
+// Coarsest level in one CTA: all `sweeps` damped-Jacobi sweeps from x = 0
+// in shared memory (same arithmetic and order as k_mg_jacobi, one launch).
+constexpr int MG_COARSE_MAX = 2048;  // cells
+
+__global__ void __launch_bounds__(1024) k_mg_coarse(MgLevel L, int sweeps, double w,
+                                                    const DevScalars *sc) {
+    if (sc && sc->done) return;
+    __shared__ double xa[MG_COARSE_MAX], xb[MG_COARSE_MAX];
+    const int nc = (int)L.nc;
+    for (int q = threadIdx.x; q < nc; q += blockDim.x) xa[q] = 0.0;
+    __syncthreads();
+    double *cur = xa, *nxt = xb;
+    for (int it = 0; it < sweeps; it++) {
+        for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+            if (L.type[q] != MG_ROW) {
+                nxt[q] = 0.0;
+                continue;
+            }
+            const double dd = L.s * (double)L.diag[q];
+            if (it == 0) {
+                nxt[q] = w * L.b[q] / dd;
+                continue;
+            }
+            nxt[q] = cur[q] + w * (L.b[q] - mg_ax(L, cur, q)) / dd;
+        }
+        __syncthreads();
+        double *t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    for (int q = threadIdx.x; q < nc; q += blockDim.x) L.x[q] = cur[q];
+}
+
 // ------------------------------------------------------------------ host --
 void mg_free(Ctx &c) {
     MgCtx *m = mg_ctx(c);
@@ -308,6 +341,11 @@ int mg_setup(Ctx &c, double scale, const int lo[3], const int hi[3], cudaStream_
 static void vcycle(const MgCtx &m, int l, const DevScalars *sc, cudaStream_t st, int64_t *launches) {
     MgLevel L = m.lv[l];
     const bool last = l == m.Lrun - 1;
+    if (last && L.nc <= MG_COARSE_MAX) {
+        k_mg_coarse<<<1, 1024, 0, st>>>(L, m.coarse, m.omega, sc);
+        (*launches)++;
+        return;
+    }
     const int pre = last ? m.coarse : m.pre;
     // damped Jacobi from x = 0, ping-pong between x and x2, ending in x
     double *cur = (pre % 2) ? L.x : L.x2, *nxt = (pre % 2) ? L.x2 : L.x;
