@@ -1014,9 +1014,19 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
         }
         LaneArgs B = A;
         B.halo_z = A.halo_y + tiles * A.geom.nsteps * TZ;
-        if (TY == 16 && TZ == 16) {
+        // DSMEM cluster kernel when its cluster shape can be scheduled here;
+        // otherwise (e.g. no 16-CTA clusters on this device) k_mic_lane2 for
+        // the rest of the process: same arithmetic, same padded tile grid
+        static bool cluster_ok = true;
+        if (TY == 16 && TZ == 16 && cluster_ok) {
             cudaError_t e = launch_mic_cluster(REV, B, st);
-            if (e != cudaErrorNotSupported) return e;
+            if (e == cudaSuccess) return e;
+            if (e != cudaErrorNotSupported) {
+                cudaGetLastError();  // a refused launch is not a sticky error
+                cluster_ok = false;
+                fprintf(stderr, "flipb200: cluster sweep unavailable (%s); using k_mic_lane2\n",
+                        cudaGetErrorString(e));
+            }
         }
         if (lane_chunk() > 0) {
             constexpr int KC = 8;
