@@ -83,6 +83,50 @@ static int dalloc(T **p, int64_t n) {
     return 0;
 }
 
+// Grow every particle-sized buffer to hold at least n particles (the
+// reference's ParticleSet has no fixed capacity).  The live particles are
+// kept; the scratch buffers (Q, radix keys/values, histograms) are simply
+// reallocated.  Called before any launch that would exceed the capacity.
+int flip::reserve_particles(Ctx &c, int64_t n) {
+    if (n <= c.cap) return 0;
+    const int64_t lim = ((int64_t)1 << 31) - 1;
+    if (n > lim) {
+        set_error("particle count exceeds the int32 indexing limit of one device");
+        return FLIP_E_CAPACITY;
+    }
+    const int64_t cap = std::min(lim, std::max(n, c.cap + c.cap / 2));
+    FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
+    for (int a = 0; a < 6; a++) {
+        double *np_ = nullptr;
+        if (int rc = dalloc(&np_, cap)) return rc;
+        if (c.n > 0)
+            FLIP_CUDA_OK(cudaMemcpyAsync(np_, c.P.a[a], sizeof(double) * c.n,
+                                         cudaMemcpyDeviceToDevice, c.st));
+        FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
+        cudaFree(c.P.a[a]);
+        c.P.a[a] = np_;
+        cudaFree(c.Q.a[a]);
+        c.Q.a[a] = nullptr;
+        if (int rc = dalloc(&c.Q.a[a], cap)) return rc;
+    }
+    int **ints[4] = {&c.keys0, &c.keys1, &c.vals0, &c.vals1};
+    for (int **q : ints) {
+        cudaFree(*q);
+        *q = nullptr;
+        if (int rc = dalloc(q, cap)) return rc;
+    }
+    cudaFree(c.hist);
+    c.hist = nullptr;
+    if (int rc = dalloc(&c.hist, radix_hist_ints(cap, c.ncells))) return rc;
+    cudaFree(c.scan_tmp);
+    c.scan_tmp = nullptr;
+    const int64_t scan_n = std::max<int64_t>(radix_hist_ints(cap, c.ncells), c.ncells + 2);
+    if (int rc = dalloc(&c.scan_tmp, scan_tmp_ints(scan_n) + 64)) return rc;
+    c.cap = cap;
+    c.keys_valid = 0;
+    return 0;
+}
+
 #define ALLOC(ptr, n)                                \
     do {                                             \
         if (int rc_ = dalloc(&(ptr), (int64_t)(n))) { \
@@ -201,7 +245,7 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     ALLOC(c->lvl_cnt, nlev + 1);
     ALLOC(c->dot_part, dot_tmp_doubles(nc));
     // the fused pairwise dot keeps a ticket word in this scratch: start at 0
-    FLIP_CUDA_OK(cudaMemset(c->dot_part, 0, sizeof(double) * dot_tmp_doubles(nc)));
+    FLIP_CUDA_OK(cudaMemsetAsync(c->dot_part, 0, sizeof(double) * dot_tmp_doubles(nc), c->st));
     ALLOC(c->wave_prog, 8);
     ALLOC(c->wave_halo, wave_halo_doubles(nx, ny, nz));
     ALLOC(c->cflags, nc);
@@ -311,10 +355,11 @@ extern "C" int flip_set_particles(flip_ctx *c, int64_t n, const double *px, cons
                                   const double *pz, const double *vx, const double *vy,
                                   const double *vz) {
     cudaSetDevice(c->device);
-    if (n < 0 || n > c->cap) {
-        set_error("particle count exceeds capacity");
-        return FLIP_E_CAPACITY;
+    if (n < 0) {
+        set_error("negative particle count");
+        return FLIP_E_ARG;
     }
+    TRY(reserve_particles(*c, n));
     const double *src[6] = {px, py, pz, vx, vy, vz};
     for (int a = 0; a < 6; a++) TRY(h2d(c->P.a[a], src[a], sizeof(double) * n, c->st));
     c->n = n;
@@ -407,10 +452,11 @@ extern "C" int flip_get_particles_f32(flip_ctx *c, float *out) {
 
 extern "C" int flip_set_particles_f32(flip_ctx *c, int64_t n, const float *in) {
     cudaSetDevice(c->device);
-    if (n < 0 || n > c->cap) {
-        set_error("particle count exceeds capacity");
-        return FLIP_E_CAPACITY;
+    if (n < 0) {
+        set_error("negative particle count");
+        return FLIP_E_ARG;
     }
+    TRY(reserve_particles(*c, n));
     float *buf;
     TRY(f32_stage(c, n, &buf));
     TRY(h2d(buf, in, sizeof(float) * 6 * n, c->st));

@@ -128,6 +128,7 @@ void mg_free(Ctx &c);
 
 void launch_set_solid_shell(Ctx &c);
 int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed);
+int reserve_particles(Ctx &c, int64_t n);
 void launch_divergence(Ctx &c, double *div_dev);
 void launch_enforce(Ctx &c, double *u, double *v, double *w);
 

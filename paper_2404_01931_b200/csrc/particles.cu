@@ -426,10 +426,7 @@ int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed) {
         FLIP_CUDA_OK(cudaMemcpyAsync(&m, &c.sc->total, sizeof(int), cudaMemcpyDeviceToHost, c.st));
         FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
         int64_t add = (int64_t)m * r.density * r.density * r.density;
-        if (c.n + add > c.cap) {
-            set_error("particle capacity exceeded while seeding");
-            return FLIP_E_CAPACITY;
-        }
+        if (int rc = reserve_particles(c, c.n + add)) return rc;
         if (add > 0) {
             k_seed_emit<<<nblocks(add), kThreads, 0, c.st>>>(c.P, c.n, cells, m, r.density, seed, c.d);
             c.launches++;

@@ -487,12 +487,14 @@ static void launch_dot_f(const LD &ld, int64_t n, double *tmp, double *out_dev, 
     int cut = pw_cut(n > 0 ? n : 1);
     int64_t nodes = (int64_t)1 << cut;
     int64_t nb1 = (nodes + 31) / 32;
-    double *p0 = tmp, *p1 = tmp + nb1;
+    // tmp[0..1]: the fused dot's ticket word, at a fixed slot so a later
+    // call with another n never finds a stale partial there; partials follow
+    double *p0 = tmp + 2, *p1 = p0 + nb1;
     // only the solver's in-loop dots may skip their work after convergence
     const bool skip = epi == EPI_CURV || epi == EPI_SIGMA_NEW;
     if (nb1 <= 1024) {
-        // ticket: the word after the partials (zeroed at allocation, re-armed by the kernel)
-        unsigned *ticket = reinterpret_cast<unsigned *>(tmp + 2 * nb1);
+        // ticket zeroed at allocation and re-armed to 0 by the last block
+        unsigned *ticket = reinterpret_cast<unsigned *>(tmp);
         k_dot_fused<LD><<<(unsigned)nb1, 256, 0, st>>>(ld, n, cut, p0, ticket, epi, sc, out_dev,
                                                        skip ? 1 : 0);
         (*launches)++;
@@ -1308,7 +1310,9 @@ __global__ void k_absmax(const double *__restrict__ a, int64_t n, unsigned long 
 
 // Device scratch for one plugin-API call, freed on scope exit.
 struct DevArena {
+    cudaStream_t st;  // the call's stream: the zero-fill is ordered before its kernels
     std::vector<void *> ptrs;
+    explicit DevArena(cudaStream_t s) : st(s) {}
     ~DevArena() {
         for (void *p : ptrs) cudaFree(p);
     }
@@ -1316,8 +1320,8 @@ struct DevArena {
     T *get(int64_t n) {
         void *p = nullptr;
         if (cudaMalloc(&p, sizeof(T) * (size_t)(n > 0 ? n : 1)) != cudaSuccess) return nullptr;
-        // zeroed: dot scratch carries the fused dot's ticket word
-        cudaMemset(p, 0, sizeof(T) * (size_t)(n > 0 ? n : 1));
+        // zeroed on the call's stream: dot scratch carries the fused dot's ticket word
+        cudaMemsetAsync(p, 0, sizeof(T) * (size_t)(n > 0 ? n : 1), st);
         ptrs.push_back(p);
         return (T *)p;
     }
@@ -1403,7 +1407,7 @@ double *upload_d(DevArena &ar, const double *h, int64_t n, cudaStream_t st) {
 extern "C" int flip_k_laplacian_matvec(int64_t n, const double *diag, const int64_t *nbr_rows,
                                        const double *x, double scale, double *y) {
     ApiStream S;
-    DevArena ar;
+    DevArena ar(S.st);
     int *nb = nullptr;
     if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
     double *dd = upload_d(ar, diag, n, S.st), *dx = upload_d(ar, x, n, S.st), *dy = ar.get<double>(n);
@@ -1418,7 +1422,7 @@ extern "C" int flip_k_laplacian_matvec(int64_t n, const double *diag, const int6
 extern "C" int flip_k_jacobi_iter(int64_t n, const double *diag, const int64_t *nbr_rows,
                                   const double *rhs, const double *x, double scale, double *out) {
     ApiStream S;
-    DevArena ar;
+    DevArena ar(S.st);
     int *nb = nullptr;
     if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
     double *dd = upload_d(ar, diag, n, S.st), *dr = upload_d(ar, rhs, n, S.st),
@@ -1435,7 +1439,7 @@ extern "C" int flip_k_gs_sweep_rows(int64_t m, const int64_t *rows, int64_t n, c
                                     const int64_t *nbr_rows, const double *rhs, double *x,
                                     double scale) {
     ApiStream S;
-    DevArena ar;
+    DevArena ar(S.st);
     int *nb = nullptr;
     if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
     double *dd = upload_d(ar, diag, n, S.st), *dr = upload_d(ar, rhs, n, S.st),
@@ -1459,7 +1463,7 @@ static int api_sweep(int mode, int64_t n, const double *diag, const int64_t *nbr
                      const double *rhs, const double *src_h, const double *precon_h, double scale,
                      double *out_h, const double *xin_h) {
     ApiStream S;
-    DevArena ar;
+    DevArena ar(S.st);
     int *nb = nullptr;
     if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
     double *dd = diag ? upload_d(ar, diag, n, S.st) : nullptr;
@@ -1503,7 +1507,7 @@ extern "C" int flip_k_mic0_apply(int64_t n, const double *precon, const int64_t 
 extern "C" int flip_k_mic0_build(int64_t n, const double *diag, const int64_t *nbr_rows,
                                  double scale, double tau, double sigma, double *precon) {
     ApiStream S;
-    DevArena ar;
+    DevArena ar(S.st);
     int *nb = nullptr;
     if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
     double *dd = upload_d(ar, diag, n, S.st), *dout = ar.get<double>(n);
@@ -1522,7 +1526,7 @@ extern "C" int flip_k_mic0_build(int64_t n, const double *diag, const int64_t *n
 
 extern "C" int flip_k_pairwise_dot(int64_t n, const double *a, const double *b, double *out) {
     ApiStream S;
-    DevArena ar;
+    DevArena ar(S.st);
     double *da = upload_d(ar, a, n, S.st), *db = b ? upload_d(ar, b, n, S.st) : nullptr;
     double *tmp = ar.get<double>(dot_tmp_doubles(n)), *res = ar.get<double>(1);
     int64_t l = 0;
@@ -1549,7 +1553,7 @@ extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, con
         return FLIP_E_CONFIG;
     }
     ApiStream S;
-    DevArena ar;
+    DevArena ar(S.st);
     int *nb = nullptr;
     if (int rc = upload_nbr(ar, nbr_rows, n, &nb, S.st)) return rc;
     double *dd = upload_d(ar, diag, n, S.st), *dr = upload_d(ar, rhs, n, S.st);

@@ -24,10 +24,10 @@ def small_spec(**kw):
     return P.SceneSpec(**base)
 
 
-def shell_state(res=8, shell=True):
+def shell_state(res=8, shell=True, dtau=None):
     """A bare device state like the reference's shell_grid fixture (8^3,
     dtau 1/8, one-cell SOLID shell, every other cell AIR, no particles)."""
-    dims = GridDims(res, res, res, 1.0 / res)
+    dims = GridDims(res, res, res, 1.0 / res if dtau is None else dtau)
     dev = Device(dims)
     if shell:
         _lib.check(_lib.LIB.flip_set_solid_shell(dev.ctx))
@@ -356,3 +356,423 @@ class TestExtrapolation:
         assert u3[4, 4, 6] == 7.0 and u3[4, 5, 5] == 7.0      # layer 2
         assert u3[4, 4, 7] == 0.0                              # beyond fill depth
         assert u3[4, 6, 4] == 7.0 and u3[4, 7, 4] == 0.0       # wall row stays zero
+
+
+# --------------------------------------------------------- test_transfer ----
+def _random_parts(n, seed):
+    rng = np.random.default_rng(seed)
+    pos, vel = rng.random((n, 3)), rng.normal(size=(n, 3))
+    return pos, vel
+
+
+class TestP2G:
+    def _p2g(self, pos, vel):
+        st = shell_state(6, shell=False)
+        set_parts(st, pos, vel)
+        stages(st, "bin", "p2g", res=6)
+        return st, st.device.known()
+
+    def test_constant_velocity_everywhere(self):            # test_transfer.py:82-93
+        pos, vel = _random_parts(500, 1)
+        vel[:] = (2.5, -1.0, 0.75)
+        st, (ku, kv, kw) = self._p2g(pos, vel)
+        u, v, w = (np.array(getattr(st.grid, c)) for c in "uvw")
+        assert np.allclose(u[ku], 2.5, atol=1e-12)
+        assert np.allclose(v[kv], -1.0, atol=1e-12)
+        assert np.allclose(w[kw], 0.75, atol=1e-12)
+        assert (u[~ku] == 0).all()
+
+    def test_single_particle_at_face_sample(self):          # test_transfer.py:95-105
+        h = 1.0 / 6.0
+        st, _ = self._p2g([[2 * h, 2.5 * h, 2.5 * h]], [[3.3, 0.0, 0.0]])
+        assert st.grid.u3()[2, 2, 2] == pytest.approx(3.3, rel=1e-15)
+
+    def test_max_principle_per_component(self):             # test_transfer.py:118-124
+        pos, vel = _random_parts(2000, 4)
+        st, (ku, _, _) = self._p2g(pos, vel)
+        u = np.array(st.grid.u)
+        assert u[ku].min() >= vel[:, 0].min() - 1e-12
+        assert u[ku].max() <= vel[:, 0].max() + 1e-12
+
+    def test_far_particle_contributes_zero(self):           # test_transfer.py:126-136
+        st, (ku, _, _) = self._p2g([[0.9, 0.9, 0.9]], [[100.0, 0.0, 0.0]])
+        assert not ku.reshape(6, 6, 7)[0, 0, 0]
+        assert st.grid.u3()[0, 0, 0] == 0.0
+
+
+class TestG2P:
+    def _state(self, seed_new=5):
+        st = shell_state(6, shell=False)
+        dev = st.device
+        rng = np.random.default_rng(seed_new)
+        z = [np.zeros(n) for n in dev.nfaces]
+        dev.set_grid(u=rng.normal(size=dev.nfaces[0]), v=z[1], w=z[2])
+        dev.set_grid_old(rng.normal(size=dev.nfaces[0]), z[1], z[2])
+        return st
+
+    def _g2p(self, st, flip):
+        stages(st, "g2p", "g2p", res=6, flip_fraction=flip)
+
+    def test_pure_pic_equals_new_field_sample(self):        # test_transfer.py:147-153
+        import oracle as O
+        st = self._state()
+        pos, vel = _random_parts(100, 6)
+        set_parts(st, pos, vel)
+        g = st.grid
+        expect = O.sample_velocity_many(O.Dimz(6, 6, 6, 1.0 / 6.0), np.array(g.u), np.array(g.v),
+                                        np.array(g.w), pos[:, 0], pos[:, 1], pos[:, 2])[0]
+        self._g2p(st, 0.0)
+        assert np.allclose(st.particles.vel_x, expect, atol=1e-14)
+
+    def test_pure_flip_with_equal_grids_is_identity(self):  # test_transfer.py:155-161
+        st = self._state()
+        st.device.set_grid_old(np.array(st.grid.u), np.array(st.grid.v), np.array(st.grid.w))
+        pos, vel = _random_parts(100, 7)
+        set_parts(st, pos, vel)
+        self._g2p(st, 1.0)
+        assert np.allclose(st.particles.vel_x, vel[:, 0], atol=1e-12)
+
+    def test_blend_arithmetic(self):                        # test_transfer.py:163-172
+        st = shell_state(6, shell=False)
+        dev = st.device
+        z = [np.zeros(n) for n in dev.nfaces]
+        dev.set_grid(u=np.full(dev.nfaces[0], 2.0), v=z[1], w=z[2])
+        dev.set_grid_old(*z)
+        set_parts(st, [[0.5, 0.5, 0.5]], [[4.0, 0.0, 0.0]])
+        self._g2p(st, 0.5)
+        assert st.particles.vel_x[0] == pytest.approx(4.0, abs=1e-14)
+
+    def test_blend_params_validation(self):                 # test_transfer.py:199-203
+        st = self._state()
+        for bad in (1.5, -0.1):
+            with pytest.raises(ValueError):
+                self._g2p(st, bad)
+
+
+class TestRoundTrip:
+    def test_constant_field_recovered_pure_pic(self):       # test_transfer.py:182-196
+        st = shell_state(6)
+        region = P.SeedRegion.box((1 / 6, 1 / 6, 1 / 6), (5 / 6, 5 / 6, 5 / 6), 2)
+        arr = (_lib.Region * 1)(region.to_c())
+        _lib.check(_lib.LIB.flip_seed_regions(st.device.ctx, 1, arr, 1))
+        st.device.bump()
+        c = (1.25, -0.5, 2.0)
+        pos = np.stack([np.array(a) for a in st.particles.arrays()[:3]], axis=1)
+        set_parts(st, pos, np.tile(c, (len(pos), 1)))
+        stages(st, "bin", "p2g", res=6)
+        g = st.grid
+        st.device.set_grid_old(np.array(g.u), np.array(g.v), np.array(g.w))
+        stages(st, "g2p", "g2p", res=6, flip_fraction=0.0)
+        p = st.particles
+        for comp, arr_ in zip(c, (p.vel_x, p.vel_y, p.vel_z)):
+            assert (np.abs(np.asarray(arr_) - comp) / abs(comp)).max() < 1e-6
+
+
+# --------------------------------------------------------- test_pressure ----
+DT, RHO = 0.01, 1000.0
+_NB6 = ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1))
+
+
+def dense_pressure(label3, u3, v3, w3, dtau, dt=DT, rho=RHO):
+    """Independent dense restatement of assemble + solve (pressure.py:147-199):
+    rows are FLUID cells in flat order; a component that touches no AIR
+    loses its lowest-index cell (pinned to zero); out-of-domain is SOLID."""
+    from scipy import ndimage
+    nz, ny, nx = label3.shape
+    fl = label3 == P.FLUID
+    comp, ncomp = ndimage.label(fl)
+    air = np.pad(label3 == P.AIR, 1)
+    near_air = np.zeros_like(fl)
+    for di, dj, dk in _NB6:
+        near_air |= air[1 + dk:1 + dk + nz, 1 + dj:1 + dj + ny, 1 + di:1 + di + nx]
+    flat = np.arange(label3.size).reshape(label3.shape)
+    pinned = set()
+    for c in range(1, ncomp + 1):
+        m = comp == c
+        if not (near_air & m).any():
+            pinned.add(int(flat[m].min()))
+    rows = [int(f) for f in flat[fl] if int(f) not in pinned]
+    index = {f: r for r, f in enumerate(rows)}
+    scale = dt / (rho * dtau * dtau)
+    A = np.zeros((len(rows), len(rows)))
+    b = np.zeros(len(rows))
+    for r, f in enumerate(rows):
+        k, j, i = np.unravel_index(f, label3.shape)
+        for di, dj, dk in _NB6:
+            a, bb, cc = i + di, j + dj, k + dk
+            inside = 0 <= a < nx and 0 <= bb < ny and 0 <= cc < nz
+            lab = label3[cc, bb, a] if inside else P.SOLID
+            if lab != P.SOLID:
+                A[r, r] += scale
+            nf = int(flat[cc, bb, a]) if inside else -1
+            if lab == P.FLUID and nf in index:
+                A[r, index[nf]] -= scale
+        b[r] = -(u3[k, j, i + 1] - u3[k, j, i] + v3[k, j + 1, i] - v3[k, j, i]
+                 + w3[k + 1, j, i] - w3[k, j, i]) / dtau
+    p = np.zeros(label3.size)
+    if rows:
+        p[rows] = np.linalg.solve(A, b)
+    return p, rows, len(pinned)
+
+
+def grid_state(label3, seed, dtau):
+    """Device state with the given labels and random velocities, walls
+    enforced (random_mask_grid / single_cell_grid, test_pressure.py:100-120)."""
+    n = label3.shape[0]
+    st = shell_state(n, shell=False, dtau=dtau)
+    dev = st.device
+    rng = np.random.default_rng(seed)
+    dev.set_grid(label=label3.reshape(-1), u=rng.normal(size=dev.nfaces[0]),
+                 v=rng.normal(size=dev.nfaces[1]), w=rng.normal(size=dev.nfaces[2]),
+                 p=np.zeros(dev.dims.ncells))
+    dev.set_dt(DT)
+    if (label3 == P.SOLID).any():
+        dev.set_known(*[np.ones(nf, np.uint8) for nf in dev.nfaces])
+        stages(st, "apply_gradient", "apply_gradient", res=n, extrapolation_layers=0)
+    return st
+
+
+def random_mask(n, seed, fraction=0.4):
+    lab = np.full((n, n, n), P.SOLID, dtype=np.uint8)
+    interior = np.full((n - 2,) * 3, P.AIR, dtype=np.uint8)
+    interior[np.random.default_rng(seed).random(interior.shape) < fraction] = P.FLUID
+    lab[1:-1, 1:-1, 1:-1] = interior
+    return lab
+
+
+def single_cell(neighbors):
+    lab = np.full((5, 5, 5), neighbors, dtype=np.uint8)
+    lab[2, 2, 2] = P.FLUID
+    return lab
+
+
+def project(st, solver, tol, max_iters, **kw):
+    n = st.device.dims.nx
+    rep = stages(st, "project", "project", res=n, solver=solver, tol=tol, max_iters=max_iters,
+                 **kw)
+    return rep, np.array(st.grid.p)
+
+
+SOLVER_NAMES = ("jacobi", "gs", "rbgs", "pcg")
+
+
+class TestSolvers:
+    @pytest.mark.parametrize("solver", SOLVER_NAMES)
+    def test_zero_rhs_zero_solution(self, solver):          # test_pressure.py:187-199
+        st = grid_state(single_cell(P.AIR), 0, 0.2)
+        z = [np.zeros(n) for n in st.device.nfaces]
+        st.device.set_grid(u=z[0], v=z[1], w=z[2])
+        rep, p = project(st, solver, 1e-6, 2000)
+        assert rep.solver_converged and (p == 0).all()
+        assert rep.solver_iterations == (0 if solver == "pcg" else 1)
+
+    @pytest.mark.parametrize("solver", SOLVER_NAMES)
+    def test_two_cell_system_matches_dense(self, solver):   # test_pressure.py:201-209
+        lab = single_cell(P.AIR)
+        lab[2, 2, 3] = P.FLUID
+        st = grid_state(lab, 0, 0.2)
+        g = st.grid
+        x, rows, _ = dense_pressure(lab, g.u3(), g.v3(), g.w3(), 0.2)
+        rep, p = project(st, solver, 1e-10, 2000)
+        assert rep.solver_converged
+        assert np.allclose(p[rows], x[rows], atol=1e-8 * max(1, np.abs(x).max()))
+
+    @pytest.mark.parametrize("solver", SOLVER_NAMES)
+    def test_8cubed_random_mask_matches_dense(self, solver):  # test_pressure.py:211-218
+        lab = random_mask(8, 7)
+        st = grid_state(lab, 8, 1 / 8)
+        g = st.grid
+        x, rows, _ = dense_pressure(lab, g.u3(), g.v3(), g.w3(), 1 / 8)
+        rep, p = project(st, solver, 1e-9, 5000)
+        assert rep.solver_converged
+        assert (np.abs(p - x) / max(1.0, np.abs(x).max())).max() < 1e-6
+
+    def test_mg_preconditioner_matches_dense(self):         # extension, same bar
+        lab = random_mask(16, 21, 0.6)
+        st = grid_state(lab, 22, 1 / 16)
+        g = st.grid
+        x, rows, _ = dense_pressure(lab, g.u3(), g.v3(), g.w3(), 1 / 16)
+        rep, p = project(st, "pcg", 1e-9, 500, precond="mg")
+        assert rep.solver_converged
+        assert (np.abs(p - x) / max(1.0, np.abs(x).max())).max() < 1e-6
+
+    def test_iteration_ordering(self):                      # test_pressure.py:220-236
+        its = {}
+        for solver in SOLVER_NAMES:
+            lab = random_mask(8, 9)
+            rep, _ = project(grid_state(lab, 10, 1 / 8), solver, 1e-8,
+                             200 if solver == "pcg" else 5000)
+            assert rep.solver_converged
+            its[solver] = rep.solver_iterations
+        assert its["gs"] < its["jacobi"]
+        assert its["pcg"] <= its["gs"] and its["pcg"] <= its["rbgs"]
+
+    def test_pcg_single_cell_one_iteration(self):          # test_pressure.py:238-243
+        lab = single_cell(P.AIR)
+        st = grid_state(lab, 0, 0.2)
+        g = st.grid
+        x, _, _ = dense_pressure(lab, g.u3(), g.v3(), g.w3(), 0.2)
+        rep, p = project(st, "pcg", 1e-6, 100)
+        assert rep.solver_converged and rep.solver_iterations == 1
+        assert p[P.flat_index(2, 2, 2, st.device.dims)] == pytest.approx(x[62], rel=1e-12)
+
+    def test_convergence_across_random_masks(self):         # test_pressure.py:245-253
+        for s in range(20):
+            lab = random_mask(6, 100 + s)
+            if not (lab == P.FLUID).any():
+                continue
+            for solver in ("jacobi", "gs"):
+                rep, _ = project(grid_state(lab, 101 + s, 1 / 6), solver, 1e-7, 5000)
+                assert rep.solver_converged
+
+    def test_sealed_two_cell_component_solvable_after_pinning(self):  # :285-292
+        lab = single_cell(P.SOLID)
+        lab[2, 2, 3] = P.FLUID
+        st = grid_state(lab, 0, 0.2)
+        rep, p = project(st, "pcg", 1e-6, 100)
+        assert rep.nrows == 1 and rep.npinned == 1 and rep.solver_converged
+        assert p[P.flat_index(2, 2, 2, st.device.dims)] == 0.0
+
+    def test_all_four_agree_on_random_masks(self):          # test_pressure.py:341-352
+        for s in range(3):
+            lab = random_mask(6, 300 + s)
+            if not (lab == P.FLUID).any():
+                continue
+            sols = [project(grid_state(lab, 301 + s, 1 / 6), sv, 1e-8, 8000)[1]
+                    for sv in SOLVER_NAMES]
+            scale = max(1.0, max(np.abs(q).max() for q in sols))
+            for a in sols:
+                for b in sols:
+                    assert (np.abs(a - b) / scale).max() < 1e-5
+
+
+class TestApplyGradient:
+    def _apply(self, st, p):
+        dev = st.device
+        dev.set_grid(p=p)
+        dev.set_known(*[np.ones(nf, np.uint8) for nf in dev.nfaces])
+        stages(st, "apply_gradient", "apply_gradient", res=dev.dims.nx, extrapolation_layers=0)
+
+    def test_uniform_pressure_all_fluid_no_change(self):    # test_pressure.py:296-306
+        lab = np.full((5, 5, 5), P.SOLID, dtype=np.uint8)
+        lab[1:-1, 1:-1, 1:-1] = P.FLUID
+        st = grid_state(lab, 12, 0.2)
+        before = np.array(st.grid.u)
+        self._apply(st, np.where(lab.reshape(-1) == P.FLUID, 3.7, 0.0))
+        assert np.allclose(st.grid.u, before, atol=1e-12)
+
+    def test_two_cell_column_face_update(self):             # test_pressure.py:308-319
+        lab = np.full((5, 5, 5), P.AIR, dtype=np.uint8)
+        lab[2, 2, 2] = lab[2, 2, 3] = P.FLUID
+        st = grid_state(lab, 0, 0.2)
+        z = [np.zeros(n) for n in st.device.nfaces]
+        st.device.set_grid(u=z[0], v=z[1], w=z[2])
+        p = np.zeros(125)
+        p.reshape(5, 5, 5)[2, 2, 3] = 50.0
+        self._apply(st, p)
+        assert st.grid.u3()[2, 2, 3] == pytest.approx(-DT / RHO * 50.0 / 0.2)
+
+    def test_solid_adjacent_faces_zeroed(self):             # test_pressure.py:321-326
+        st = grid_state(random_mask(6, 13), 14, 1 / 6)
+        self._apply(st, np.zeros(216))
+        u3 = st.grid.u3()
+        assert np.all(u3[:, :, :2] == 0) and np.all(u3[:, :, -2:] == 0)
+
+    def test_projection_kills_divergence(self):             # test_pressure.py:328-338
+        lab = random_mask(8, 14)
+        st = grid_state(lab, 15, 1 / 8)
+        fl = (lab.reshape(-1) == P.FLUID)
+        rhs_max = max(1.0, np.abs(P.divergence_field(st)[fl]).max())
+        tol = 1e-8
+        rep = stages(st, "project", "project", res=8, tol=tol, max_iters=500)
+        assert rep.solver_converged
+        self._apply(st, np.array(st.grid.p))
+        div = P.divergence_field(st)
+        assert np.abs(div[fl]).max() <= 100 * tol * rhs_max
+
+
+# ---------------------------------------------------------- test_binning ----
+class TestBinParticles:
+    def _bin(self, pos):
+        st = shell_state(6, shell=False)
+        set_parts(st, pos)
+        stages(st, "bin", "classify", res=6)
+        return st
+
+    def test_single_cell_keeps_order(self):                 # test_binning.py:98-107
+        pos = 0.05 + np.random.default_rng(3).random((20, 3)) * 0.05
+        st = self._bin(pos)
+        assert np.array_equal(st.particles.pos_x, pos[:, 0])
+        assert st.hash.offset[0] == 0 and st.hash.count[0] == 20
+        assert np.asarray(st.hash.fluid_cells).tolist() == [0]
+
+    def test_empty_set(self):                               # test_binning.py:109-112
+        st = self._bin(np.zeros((0, 3)))
+        assert st.particles.count == 0
+        assert int(np.asarray(st.hash.count).sum()) == 0 and len(st.hash.fluid_cells) == 0
+
+    def test_matches_stable_sort_byte_identical(self):      # test_binning.py:114-121
+        pos, vel = _random_parts(10**5, 5)
+        st = shell_state(6, shell=False)
+        set_parts(st, pos, vel)
+        stages(st, "bin", "classify", res=6)
+        i, j, k = (np.minimum(np.floor(pos[:, a] * 6).astype(np.int64), 5) for a in range(3))
+        perm = np.argsort(i + 6 * (j + 6 * k), kind="stable")
+        want = np.concatenate([pos, vel], axis=1)[perm]
+        for a, got in enumerate(st.particles.arrays()):
+            assert np.asarray(got).tobytes() == np.ascontiguousarray(want[:, a]).tobytes()
+
+    def test_hash_invariants(self):                         # test_binning.py:123-139
+        pos, _ = _random_parts(5000, 6)
+        st = self._bin(pos)
+        h = st.hash
+        cnt, off = np.asarray(h.count), np.asarray(h.offset)
+        assert np.array_equal(off[1:], np.cumsum(cnt)[:-1]) and off[0] == 0
+        assert off[-1] + cnt[-1] == st.particles.count
+        assert np.array_equal(h.fluid_cells, np.flatnonzero(cnt > 0))
+        assert np.array_equal(np.sort(st.particles.pos_x), np.sort(pos[:, 0]))
+        p = st.particles
+        i, j, k = (np.minimum(np.floor(np.asarray(a) * 6).astype(np.int64), 5)
+                   for a in (p.pos_x, p.pos_y, p.pos_z))
+        cells = i + 6 * (j + 6 * k)
+        for c in np.asarray(h.fluid_cells)[:50]:
+            assert (cells[h.segment(int(c))] == c).all()
+
+
+def test_particle_buffers_grow_past_initial_capacity():
+    """The reference's ParticleSet has no capacity; the device context grows
+    its particle buffers on set/seed, keeping live particles."""
+    dims = GridDims(8, 8, 8, 1.0 / 8)
+    dev = Device(dims, capacity=16)
+    _lib.check(_lib.LIB.flip_set_solid_shell(dev.ctx))
+    pos, vel = _random_parts(40, 11)
+    pos = 0.125 + pos * 0.75
+    dev.set_particles([*pos.T, *vel.T])
+    region = P.SeedRegion.box((0.125, 0.125, 0.125), (0.5, 0.5, 0.5), 2)
+    _lib.check(_lib.LIB.flip_seed_regions(dev.ctx, 1, (_lib.Region * 1)(region.to_c()), 3))
+    dev.bump()
+    parts = dev.particles()
+    assert len(parts[0]) == 40 + 27 * 8
+    assert np.array_equal(parts[0][:40], pos[:, 0]) and np.array_equal(parts[3][:40], vel[:, 0])
+    st = sim.SimState(grid=MacGrid(dev, "grid"),
+                      grid_old=MacGrid(dev, "old", np.zeros(dims.ncells),
+                                       np.array(dev.grid_array("label"))),
+                      particles=ParticleSet(device=dev), hash=SpaceHash(device=dev), device=dev)
+    P.step(st, small_spec(res=8))
+    assert int(np.asarray(st.hash.count).sum()) == st.particles.count
+
+
+def test_solver_api_independent_of_call_order():
+    """Standalone solves with different n back to back (the fused dot's
+    scratch must not carry state from an earlier call)."""
+    for n, seed in ((8, 1), (6, 2), (8, 3), (5, 4), (8, 5)):
+        lab = random_mask(n, seed)
+        if not (lab == P.FLUID).any():
+            continue
+        st = grid_state(lab, seed + 50, 1.0 / n)
+        g = st.grid
+        x, _, _ = dense_pressure(lab, g.u3(), g.v3(), g.w3(), 1.0 / n)
+        for pre in ("jacobi", "mic0", "none"):
+            rep, p = project(st, "pcg", 1e-10, 500, precond=pre)
+            assert rep.solver_converged
+            assert (np.abs(p - x) / max(1.0, np.abs(x).max())).max() < 1e-6
