@@ -147,7 +147,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
                     c->has_air, c->cell_of_row, c->nbr, c->diagd, c->rhs, c->x, c->r, c->z, c->s,
                     c->q, c->tq, c->precon, c->xtmp, c->u64_scratch, c->lvl, c->lvl_rows,
-                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->lrow, c->posL, c->laneA, c->laneB, c->laneC, c->laneD, c->sc, c->f32_buf};
+                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->lrow, c->posL, c->laneA, c->laneB, c->laneC, c->laneD, c->sc, c->f32_buf, c->nb_meta, c->nb_dy, c->nb_dz};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
@@ -227,6 +227,9 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     ALLOC(c->has_air, nc);
     ALLOC(c->cell_of_row, nc);
     ALLOC(c->nbr, 6 * nc);
+    ALLOC(c->nb_meta, nc);
+    ALLOC(c->nb_dy, nc);
+    ALLOC(c->nb_dz, nc);
     ALLOC(c->diagd, nc);
     ALLOC(c->rhs, nc);
     ALLOC(c->x, nc);

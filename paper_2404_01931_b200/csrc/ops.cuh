@@ -30,6 +30,7 @@ struct DevScalars {
     int nlevels;
     int row_lo[3], row_hi[3];           // bounding box of the pressure rows
     int pad;
+    unsigned upd_ticket;                // k_pcg_update's last-block ticket (re-armed to 0)
 };
 
 // CUDA-event bracketing of one kernel class (bench roofline evidence).
@@ -52,6 +53,9 @@ struct Ctx {
     int64_t slab_c0 = 0, slab_c1 = -1;  // reseed cell range (flip_set_slab); -1: all
     void *f32_buf = nullptr;           // snapshot staging (flip_*_particles_f32)
     void *mg = nullptr;                // multigrid levels (mg.cu), allocated on first use
+    unsigned short *nb_meta = nullptr; // compact PCG stencil (k_compact_nbr), nc entries
+    unsigned *nb_dy = nullptr;
+    int2 *nb_dz = nullptr;
     size_t f32_cap = 0;
     ParticlePtrs P{}, Q{};  // current and back particle buffers
     double *u = nullptr, *v = nullptr, *w = nullptr, *p = nullptr;

@@ -266,6 +266,8 @@ __device__ __forceinline__ int64_t pw_split(int64_t n) {
     return n2 - n2 % 8;
 }
 
+constexpr int kDotBlocksPerSM = 5;  // 48 registers: the batched leaf loads do not spill
+
 // Element loaders for the pairwise dot: ld(i) returns the i-th summand and
 // is called exactly once per element, so a loader may also produce a vector
 // (the fused matvec and lane-gather variants below).
@@ -284,16 +286,29 @@ __device__ __forceinline__ double pw_leaf8(const LD &ld, int64_t s, int64_t len,
             for (int64_t i = 0; i < len; i++) res += ld(s + i);
         return res;
     }
-    // len <= 128: a lane owns at most 16 summands; load them all first (the
-    // loads are independent), then accumulate in numpy's order
+    // len <= 128: a lane owns at most 16 summands.  Two batches of 8 loads (register count low enough for the dot's
+    // occupancy); the accumulation order is unchanged.  The loads are
+    // unconditional, at a clamped (always valid) index, and the unused
+    // values are dropped afterwards: a guarded load compiles to a branch per
+    // element and serialises the round trips.  A loader with a side effect
+    // (z[i] = ...) repeats the same store for the clamped index.
     const int cntv = (int)(len / 8);
-    double v[16];
+    double r;
+    {
+        double v[8];
 #pragma unroll
-    for (int k = 0; k < 16; k++) v[k] = k < cntv ? ld(s + g + 8 * k) : 0.0;
-    double r = v[0];
+        for (int k = 0; k < 8; k++) v[k] = ld(s + g + 8 * min(k, cntv - 1));
+        r = v[0];
 #pragma unroll
-    for (int k = 1; k < 16; k++)
-        if (k < cntv) r += v[k];
+        for (int k = 1; k < 8; k++) r = k < cntv ? r + v[k] : r;
+    }
+    if (cntv > 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = ld(s + g + 8 * min(k + 8, cntv - 1));
+#pragma unroll
+        for (int k = 0; k < 8; k++) r = k + 8 < cntv ? r + v[k] : r;
+    }
     const int64_t m = (int64_t)cntv * 8;
     r = r + __shfl_xor_sync(mask, r, 1, 8);
     r = r + __shfl_xor_sync(mask, r, 2, 8);
@@ -403,43 +418,59 @@ __global__ void k_dot_tree(const double *__restrict__ in, int64_t cnt, double *_
 // finish (threadfence + ticket) runs k_dot_tree's perfect-tree reduction and
 // the epilogue, then re-arms the ticket.  Same summation order.
 template <class LD>
-__global__ void k_dot_fused(LD ld, int64_t n, int cut, double *__restrict__ part,
-                            unsigned *ticket, int epi, DevScalars *sc, double *final_out,
-                            int skip_when_done) {
+__global__ void __launch_bounds__(256, kDotBlocksPerSM)
+k_dot_fused(LD ld, int64_t n, int cut, double *__restrict__ part, unsigned *ticket, int epi,
+            DevScalars *sc, double *final_out, int skip_when_done) {
     if (skip_when_done && sc->done) return;
-    __shared__ double sv[32];
+    __shared__ double sv[8];
     __shared__ double sv2[1024];
     __shared__ bool last;
-    int64_t nodes = (int64_t)1 << cut;
-    int64_t node = (int64_t)blockIdx.x * 32 + (threadIdx.x >> 3);
-    int g = threadIdx.x & 7;
-    double val = 0.0;
-    if (node < nodes) {
-        int64_t s0 = 0, len = n;
-        for (int lvl = cut - 1; lvl >= 0; lvl--) {
-            int64_t n2 = pw_split(len);
-            if ((node >> lvl) & 1) {
-                s0 += n2;
-                len -= n2;
-            } else {
-                len = n2;
+    const int64_t nodes = (int64_t)1 << cut;
+    const int64_t nparts = (nodes + 31) / 32;  // one partial per 32 nodes
+    const int g = threadIdx.x & 7;
+    // the grid is sized to the resident block slots; each block walks node
+    // blocks of 32 (no wave quantisation, one ticket per block at the end)
+    for (int64_t pb = blockIdx.x; pb < nparts; pb += gridDim.x) {
+        const int64_t node = pb * 32 + (threadIdx.x >> 3);
+        double val = 0.0;
+        if (node < nodes) {
+            int64_t s0 = 0, len = n;
+            for (int lvl = cut - 1; lvl >= 0; lvl--) {
+                int64_t n2 = pw_split(len);
+                if ((node >> lvl) & 1) {
+                    s0 += n2;
+                    len -= n2;
+                } else {
+                    len = n2;
+                }
             }
+            val = pw_node8<2>(ld, s0, len, g);
         }
-        val = pw_node8<2>(ld, s0, len, g);
+        // the perfect tree over these 32 nodes (pairs 2i, 2i+1 first):
+        // levels 1-2 inside the warp (node sums sit in lanes 0, 8, 16, 24;
+        // a + b == b + a exactly, so lane 0 holds the left+right bits),
+        // levels 3-5 over the 8 warp sums; levels that do not exist
+        // (nodes < 32) are skipped
+        if (nodes >= 2) val = val + __shfl_xor_sync(0xffffffffu, val, 8);
+        if (nodes >= 4) val = val + __shfl_xor_sync(0xffffffffu, val, 16);
+        if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = val;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int cw = nodes >= 32 ? 8 : (nodes >= 4 ? (int)(nodes / 4) : 1);
+            for (int st = 1; st < cw; st <<= 1)
+                for (int i = 0; i + st < cw; i += 2 * st) sv[i] = sv[i] + sv[i + st];
+            part[pb] = sv[0];
+        }
+        __syncthreads();
     }
-    if (g == 0) sv[threadIdx.x >> 3] = val;
-    __syncthreads();
-    int cnt = nodes < 32 ? (int)nodes : 32;
     if (threadIdx.x == 0) {
-        for (int st = 1; st < cnt; st <<= 1)
-            for (int i = 0; i + st < cnt; i += 2 * st) sv[i] = sv[i] + sv[i + st];
-        part[blockIdx.x] = sv[0];
         __threadfence();
         last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
-    const int m = (int)gridDim.x;
+    // perfect tree over the nparts (<= 1024, a power of two) partials
+    const int m = (int)nparts;
     for (int i = threadIdx.x; i < m; i += blockDim.x) sv2[i] = __ldcg(part + i);
     __syncthreads();
     for (int st = 1; st < m; st <<= 1) {
@@ -495,8 +526,9 @@ static void launch_dot_f(const LD &ld, int64_t n, double *tmp, double *out_dev, 
     if (nb1 <= 1024) {
         // ticket zeroed at allocation and re-armed to 0 by the last block
         unsigned *ticket = reinterpret_cast<unsigned *>(tmp);
-        k_dot_fused<LD><<<(unsigned)nb1, 256, 0, st>>>(ld, n, cut, p0, ticket, epi, sc, out_dev,
-                                                       skip ? 1 : 0);
+        const unsigned grid = (unsigned)std::min<int64_t>(nb1, 148 * kDotBlocksPerSM);
+        k_dot_fused<LD><<<grid, 256, 0, st>>>(ld, n, cut, p0, ticket, epi, sc, out_dev,
+                                              skip ? 1 : 0);
         (*launches)++;
         return;
     }
@@ -533,6 +565,13 @@ struct SysView {
     const double *diag;
     const double *rhs;
     double scale;          // host value, or taken from sc->... when from_dt
+    // optional compact stencil of a grid-assembled system (k_compact_nbr):
+    // meta = 6 presence bits (nbr order -x,+x,-y,+y,-z,+z) | diag count << 8;
+    // -x/+x are rows r-1/r+1, dy = (r - row(-y)) | (row(+y) - r) << 16,
+    // dz = (r - row(-z), row(+z) - r).  14 bytes per row instead of 32.
+    const unsigned short *meta = nullptr;
+    const unsigned *dy = nullptr;
+    const int2 *dz = nullptr;
 };
 
 __device__ __forceinline__ double nbr_sum(const int *__restrict__ nbr, int64_t ldn, int64_t r,
@@ -564,6 +603,47 @@ __global__ void k_matvec(SysView S, const double *__restrict__ x, double *__rest
     if (resmax) {
         for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(resmax, m);
+    }
+}
+
+// Compact stencil of a system assembled on the grid (k_assemble_rows): rows
+// are numbered in cell order, so an x-neighbour row is r -/+ 1 and a
+// y-neighbour lies at most nx rows away.  Exact: diag holds a small integer.
+__global__ void k_compact_nbr(SysView S, unsigned short *__restrict__ meta,
+                              unsigned *__restrict__ dy, int2 *__restrict__ dz) {
+    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+        unsigned m = (unsigned)S.diag[r] << 8;
+        int nb[6];
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+            nb[q] = S.nbr[q * S.ldn + r];
+            if (nb[q] >= 0) m |= 1u << q;
+        }
+        meta[r] = (unsigned short)m;
+        const unsigned ym = nb[2] >= 0 ? (unsigned)(r - nb[2]) : 0u;
+        const unsigned yp = nb[3] >= 0 ? (unsigned)(nb[3] - r) : 0u;
+        dy[r] = ym | yp << 16;
+        dz[r] = make_int2(nb[4] >= 0 ? (int)(r - nb[4]) : 0, nb[5] >= 0 ? (int)(nb[5] - r) : 0);
+    }
+}
+
+// k_matvec (y = A x) over the compact stencil; same additions in the same
+// order as nbr_sum, so the result is bit-identical.
+__global__ void __launch_bounds__(256)
+k_matvec_c(SysView S, const double *__restrict__ x, double *__restrict__ y, const DevScalars *sc) {
+    if (sc->done) return;
+    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+        const unsigned m = S.meta[r];
+        const unsigned d = S.dy[r];
+        const int2 z = S.dz[r];
+        double s = 0.0;
+        if (m & 1u) s = s + x[r - 1];
+        if (m & 2u) s = s + x[r + 1];
+        if (m & 4u) s = s + x[r - (int64_t)(d & 0xffffu)];
+        if (m & 8u) s = s + x[r + (int64_t)(d >> 16)];
+        if (m & 16u) s = s + x[r - (int64_t)z.x];
+        if (m & 32u) s = s + x[r + (int64_t)z.y];
+        y[r] = S.scale * ((double)(m >> 8) * x[r] - s);
     }
 }
 
@@ -855,29 +935,10 @@ __global__ void k_check_diag_final(SysView S, DevScalars *sc, const unsigned lon
 // x += alpha s; r -= alpha q; res = max|r|  (pressure.py:321-323)
 // (rL, posL): also scatter r into the MIC(0) sweep's lane layout
 // (k_rows_to_lane fused).
-__global__ void k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
-                             const double *__restrict__ s, const double *__restrict__ q,
-                             DevScalars *sc, double *__restrict__ rL, const int *__restrict__ posL) {
-    if (sc->done) return;
-    double alpha = sc->alpha;
-    double m = 0.0;
-    for (int64_t i = gtid(); i < n; i += gstride()) {
-        x[i] = x[i] + alpha * s[i];
-        double ri = r[i] - alpha * q[i];
-        r[i] = ri;
-        if (rL) rL[posL[i]] = ri;
-        m = fmax(m, fabs(ri));
-    }
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(&sc->res_bits, m);
-}
-
-// convergence test after an iteration (pressure.py:324-326 / 211-213)
-__global__ void k_iter_check(DevScalars *sc, int64_t max_iters, double *history) {
-    if (sc->done) return;
+__device__ __forceinline__ void iter_check_body(DevScalars *sc, int64_t max_iters,
+                                                double *history, double res) {
     int it = sc->iter + 1;
     sc->iter = it;
-    double res = __longlong_as_double((long long)sc->res_bits);
     sc->res = res;
     sc->res_bits = 0;
     if (history) history[it - 1] = res;
@@ -888,6 +949,74 @@ __global__ void k_iter_check(DevScalars *sc, int64_t max_iters, double *history)
         sc->done = 1;
         sc->converged = 0;
     }
+}
+
+// x += alpha s; r -= alpha q; max|r| (pressure.py:321-326), four rows in
+// flight per thread; one max per block, and the block that finishes last
+// runs the convergence test (k_iter_check's body), so the PCG loop needs no
+// separate check launch.
+__global__ void __launch_bounds__(256)
+k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
+             const double *__restrict__ s, const double *__restrict__ q, DevScalars *sc,
+             double *__restrict__ rL, const int *__restrict__ posL, int64_t max_iters,
+             double *history) {
+    if (sc->done) return;
+    __shared__ double wm[8];
+    __shared__ bool last;
+    const double alpha = sc->alpha;
+    const int64_t stride = gstride();
+    double m = 0.0;
+    int64_t i = gtid();
+    for (; i + 3 * stride < n; i += 4 * stride) {
+        double xs[4], ss[4], rs[4], qs[4];
+        int ps[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t j = i + u * stride;
+            xs[u] = x[j];
+            ss[u] = s[j];
+            rs[u] = r[j];
+            qs[u] = q[j];
+            ps[u] = rL ? posL[j] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t j = i + u * stride;
+            x[j] = xs[u] + alpha * ss[u];
+            const double ri = rs[u] - alpha * qs[u];
+            r[j] = ri;
+            if (rL) rL[ps[u]] = ri;
+            m = fmax(m, fabs(ri));
+        }
+    }
+    for (; i < n; i += stride) {
+        x[i] = x[i] + alpha * s[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        if (rL) rL[posL[i]] = ri;
+        m = fmax(m, fabs(ri));
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmax(m, wm[w]);
+        if (m > 0.0) atomic_max_nonneg(&sc->res_bits, m);
+        __threadfence();
+        last = atomicAdd(&sc->upd_ticket, 1u) == gridDim.x - 1;
+        if (last) {
+            sc->upd_ticket = 0u;
+            const double res = __longlong_as_double(
+                (long long)atomicAdd(&sc->res_bits, 0ull));
+            iter_check_body(sc, max_iters, history, res);
+        }
+    }
+}
+
+// convergence test after an iteration (pressure.py:324-326 / 211-213)
+__global__ void k_iter_check(DevScalars *sc, int64_t max_iters, double *history) {
+    if (sc->done) return;
+    iter_check_body(sc, max_iters, history, __longlong_as_double((long long)sc->res_bits));
 }
 
 // z = r * inv_diag (Jacobi preconditioner, pressure.py:289-293) or z = r
@@ -1007,6 +1136,8 @@ static cudaError_t g_sweep_launch_err = cudaSuccess;
 
 // fused: the lane path's r -> L and L -> z conversions are done by the
 // caller's k_pcg_update and z.r dot (r already in Lb.rL, z left in Lb.zL).
+// (Scattering z into row order from inside the backward sweep instead was
+// measured slower: +36 us per sweep for -21 us in the dot at 256^3.)
 static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                      const SweepLevels &LV, const double *r, double *z, DevScalars *sc,
                      cudaStream_t st, int64_t *launches, bool fused = false) {
@@ -1103,15 +1234,18 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                     launch_dot_f(LdMatvecDot{S, B.s, B.q}, n, B.dot_tmp, nullptr, EPI_CURV, sc,
                                  st, launches);
                 } else {
-                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
-                                                              nullptr, sc, 1);
+                    if (S.meta)
+                        k_matvec_c<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, sc);
+                    else
+                        k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
+                                                                  nullptr, sc, 1);
                     launch_dot(B.s, B.q, n, B.dot_tmp, nullptr, EPI_CURV, sc, st, launches);
                     (*launches)++;
                 }
                 k_pcg_update<<<nblocks(n), kThreads, 0, st>>>(n, B.x, B.r, B.s, B.q, sc,
                                                               lane ? LV.lane->rL : nullptr,
-                                                              lane ? LV.lane->posL : nullptr);
-                k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
+                                                              lane ? LV.lane->posL : nullptr,
+                                                              cfg.max_iters, cfg.history);
                 apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
                 if (lane)
                     launch_dot_f(LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, n, B.dot_tmp,
@@ -1119,7 +1253,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 else
                     launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA_NEW, sc, st, launches);
                 k_pcg_dir<<<nblocks(n), kThreads, 0, st>>>(n, B.s, B.z, sc);
-                *launches += 3;
+                *launches += 2;  // update (with the convergence test) + dir
             } else {  // pressure.py:209-213
                 if (cfg.solver == FLIP_SOLVER_JACOBI) {
                     k_jacobi<<<nblocks(n), kThreads, 0, st>>>(S, B.x, B.xtmp, sc, 1);
@@ -1204,6 +1338,14 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     // scale = dt / (rho * dtau**2) (pressure.py:164), same IEEE division as the reference
     double scale = dt / prm.rho_dtau2_h;
     SysView S{n, c.cell_of_row, c.nbr, nc, c.diagd, c.rhs, scale};
+    static const bool plain_mv = getenv("FLIPB200_PLAIN_MATVEC") != nullptr;
+    if (prm.solver == FLIP_SOLVER_PCG && n > 0 && c.d.nx < 32768 && !plain_mv) {
+        k_compact_nbr<<<nblocks(n), kThreads, 0, st>>>(S, c.nb_meta, c.nb_dy, c.nb_dz);
+        c.launches++;
+        S.meta = c.nb_meta;
+        S.dy = c.nb_dy;
+        S.dz = c.nb_dz;
+    }
     // sequential sweeps (GS, MIC(0)) run as the pipelined wavefront over the
     // rows' bounding box; FLIPB200_LEVEL_SWEEPS=1 selects the level-scheduled
     // cooperative fallback (same results, used to cross-check)
