@@ -67,6 +67,31 @@ __device__ __forceinline__ double poll_local(const double *p) {
     return __longlong_as_double((long long)v);
 }
 
+// Global face slot, polled without back-off: on this path a consumer waits
+// for a value its producer has just published, so every sleep quantum lands
+// on the sweep's critical path.
+__device__ __forceinline__ double poll_spin_gpu(const double *p) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    } while (v == WAVE_PENDING);
+    return __longlong_as_double((long long)v);
+}
+
+// one non-blocking read of a ring slot (the pending marker if not yet stored)
+__device__ __forceinline__ double peek_local(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.cluster.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(smem_addr(p)) : "memory");
+    return __longlong_as_double((long long)v);
+}
+
+// Face value for this step from a slot read one step earlier: the read's
+// latency overlaps the previous step, and only a slot that was still
+// pending then is polled again.
+__device__ __forceinline__ double take_face(double pre, const double *p) {
+    return is_pending(pre) ? poll_local(p) : pre;
+}
+
 // cluster ticket -> (bq, cq) in anti-diagonal order over the cluster grid
 __device__ __forceinline__ void cluster_tile(int t, int CB, int CC, int &bq, int &cq) {
     int d = 0;
@@ -193,7 +218,7 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
         };
 #pragma unroll
         for (int u = 0; u < UH; u++) fetch(u + 1, u);
-        if (in) sval[1][in_row][in_col] = D < nsteps ? poll_ready(in + (int64_t)D * W) : nz0;
+        if (in) sval[1][in_row][in_col] = D < nsteps ? poll_spin_gpu(in + (int64_t)D * W) : nz0;
         for (int s0 = 0; s0 < nsteps; s0 += UH) {
 #pragma unroll
             for (int u = 0; u < UH; u++) {
@@ -208,7 +233,7 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 const int cur = s & 1, prv = cur ^ 1;
                 if (in) {
                     double v = hr[u];
-                    if (is_pending(v)) v = poll_ready(in + (int64_t)(s + 1 + D) * W);
+                    if (is_pending(v)) v = poll_spin_gpu(in + (int64_t)(s + 1 + D) * W);
                     sval[cur][in_row][in_col] = v;
                     fetch(s + 1 + UH, u);
                 }
@@ -236,6 +261,9 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
         const int64_t base = (int64_t)tile * nsteps * TP + t;
         double *dstL = A.dst + base;
         double pv = nz0;
+        // face slots of the next step, read one step ahead (take_face)
+        double ypre = yin && DY < nsteps ? peek_local(yring + DY * TZ + kk) : pend;
+        double zpre = zin && DZ < nsteps ? peek_local(zring + DZ * TY + jj) : pend;
         const double sc = A.scale;
         if constexpr (NB == 0) {
             // operands straight into registers KC steps ahead (coalesced 8-byte
@@ -260,8 +288,14 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                     const double a = av[u], pr = bv[u];
                     load(s + KC, u);
                     double yv = sval[prv][yr][yc], zv = sval[prv][zr][zc];
-                    if (yin) yv = s + DY < nsteps ? poll_local(yring + (s + DY) * TZ + kk) : nz0;
-                    if (zin) zv = s + DZ < nsteps ? poll_local(zring + (s + DZ) * TY + jj) : nz0;
+                    if (yin) {
+                        yv = s + DY < nsteps ? take_face(ypre, yring + (s + DY) * TZ + kk) : nz0;
+                        if (s + 1 + DY < nsteps) ypre = peek_local(yring + (s + 1 + DY) * TZ + kk);
+                    }
+                    if (zin) {
+                        zv = s + DZ < nsteps ? take_face(zpre, zring + (s + DZ) * TY + jj) : nz0;
+                        if (s + 1 + DZ < nsteps) zpre = peek_local(zring + (s + 1 + DZ) * TY + jj);
+                    }
                     const bool row = valid && present(a);
                     double o;
                     if (!REV) {  // _core.pyx:322-332
@@ -300,12 +334,22 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
                 const int idx = REV ? cnt - 1 - u : u;
                 const double a = ab[idx * TP], pr = pb[idx * TP];
                 double yv = sval[prv][yr][yc], zv = sval[prv][zr][zc];
-                if (yin) yv = s + DY < nsteps ? poll_local(yring + (s + DY) * TZ + kk) : nz0;
-                if (zin) zv = s + DZ < nsteps ? poll_local(zring + (s + DZ) * TY + jj) : nz0;
-                if (A.trace && !REV && t == 0 && tile < 8 && s < 300) {
+                if (yin) {
+                    yv = s + DY < nsteps ? take_face(ypre, yring + (s + DY) * TZ + kk) : nz0;
+                    if (s + 1 + DY < nsteps) ypre = peek_local(yring + (s + 1 + DY) * TZ + kk);
+                }
+                if (zin) {
+                    zv = s + DZ < nsteps ? take_face(zpre, zring + (s + DZ) * TY + jj) : nz0;
+                    if (s + 1 + DZ < nsteps) zpre = peek_local(zring + (s + 1 + DZ) * TY + jj);
+                }
+                if (A.trace && !REV && t == 0 && (s == 0 || (tile < 8 && s < 300))) {
                     unsigned long long g;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-                    A.trace[20000 + tile * 300 + s] = g;
+                    if (tile < 8 && s < 300) A.trace[20000 + tile * 300 + s] = g;
+                    if (s == 0) {
+                        A.trace[4 * tile + 2] = g;
+                        A.trace[4 * tile + 3] = (unsigned long long)b << 16 | (unsigned)c;
+                    }
                 }
                 const bool row = valid && present(a);
                 double o;
