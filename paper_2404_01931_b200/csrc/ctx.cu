@@ -638,7 +638,7 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
                 stage_g2p(*c, *prm);
                 break;
             case FLIP_STAGE_RESEED:
-                stage_reseed(*c, *prm);
+                if (int rc = stage_reseed(*c, *prm)) return rc;
                 reseed_ran = true;
                 break;
         }

@@ -120,7 +120,7 @@ void stage_force(Ctx &c, const flip_step_params &prm); // body force + enforce
 int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep);  // syncs
 void stage_apply_gradient(Ctx &c, const flip_step_params &prm);
 void stage_g2p(Ctx &c, const flip_step_params &prm);
-void stage_reseed(Ctx &c, const flip_step_params &prm);
+int stage_reseed(Ctx &c, const flip_step_params &prm);
 void launch_particle_cells(Ctx &c, int *out);
 void launch_set_solid_box(Ctx &c, const int b[6]);
 void launch_particles_f32(Ctx &c, float *buf, bool to_f32);

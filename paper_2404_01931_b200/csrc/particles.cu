@@ -310,14 +310,8 @@ __global__ void k_reseed_emit(ParticlePtrs Q, Dims d, const int *__restrict__ co
     }
 }
 
-void stage_reseed(Ctx &c, const flip_step_params &prm) {
+int stage_reseed(Ctx &c, const flip_step_params &prm) {
     int *new_count = c.count2, *new_offset = c.offset2, *nadd = c.nadd;
-    if (!c.keys_valid && c.n > 0) {  // cell of each binned particle from the hash
-        k_cells_from_hash<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.offset, c.ncells, c.keys0);
-        c.keys_sorted = c.keys0;
-        c.keys_valid = 1;
-        c.launches++;
-    }
     cudaMemsetAsync(&c.sc->reseed_changed, 0, sizeof(int), c.st);
     const int64_t c1 = c.slab_c1 < 0 ? c.ncells : c.slab_c1;
     k_reseed_count<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.count, c.label, c.ncells,
@@ -326,6 +320,23 @@ void stage_reseed(Ctx &c, const flip_step_params &prm) {
     exclusive_scan(ArrayIn{new_count}, c.ncells, new_offset, new_offset + c.ncells, c.scan_tmp,
                    c.st);
     c.launches += 4;
+    // Below the MAX_PER_CELL-per-cell bound a caller-chosen capacity can be
+    // exceeded: read the new total and grow the particle buffers first
+    // (growing drops the cell keys, rebuilt from the hash below).
+    if (c.cap < (int64_t)MAX_PER_CELL * c.ncells) {
+        int total = 0;
+        FLIP_CUDA_OK(cudaMemcpyAsync(&total, new_offset + c.ncells, sizeof(int),
+                                     cudaMemcpyDeviceToHost, c.st));
+        FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
+        if (total > c.cap)
+            if (int rc = reserve_particles(c, total)) return rc;
+    }
+    if (!c.keys_valid && c.n > 0) {  // cell of each binned particle from the hash
+        k_cells_from_hash<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.offset, c.ncells, c.keys0);
+        c.keys_sorted = c.keys0;
+        c.keys_valid = 1;
+        c.launches++;
+    }
     if (c.n > 0) {
         k_reseed_copy<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.Q, c.n, c.keys_sorted, c.offset,
                                                            new_offset, c.sc);
@@ -336,6 +347,7 @@ void stage_reseed(Ctx &c, const flip_step_params &prm) {
                                                             c.w, c.sc);
     c.launches++;
     // the host swaps P<->Q and the hash buffers after reading reseed_changed
+    return 0;
 }
 
 // --------------------------------------------------------------- seeding --

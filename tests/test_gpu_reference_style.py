@@ -776,3 +776,30 @@ def test_solver_api_independent_of_call_order():
             rep, p = project(st, "pcg", 1e-10, 500, precond=pre)
             assert rep.solver_converged
             assert (np.abs(p - x) / max(1.0, np.abs(x).max())).max() < 1e-6
+
+
+def test_reseed_grows_past_user_capacity():
+    """A capacity below the 12-per-cell bound: reseed grows the buffers
+    instead of writing past them, and matches the default-capacity run."""
+    dims = GridDims(8, 8, 8, 1.0 / 8)
+    region = P.SeedRegion.box((0.125, 0.125, 0.125), (0.625, 0.625, 0.625), 1)
+    outs = []
+    for cap in (64, 0):
+        dev = Device(dims, capacity=cap)
+        _lib.check(_lib.LIB.flip_set_solid_shell(dev.ctx))
+        _lib.check(_lib.LIB.flip_seed_regions(dev.ctx, 1, (_lib.Region * 1)(region.to_c()), 4))
+        dev.bump()
+        st = sim.SimState(grid=MacGrid(dev, "grid"),
+                          grid_old=MacGrid(dev, "old", np.zeros(dims.ncells),
+                                           np.array(dev.grid_array("label"))),
+                          particles=ParticleSet(device=dev), hash=SpaceHash(device=dev),
+                          device=dev)
+        spec = small_spec(res=8, density=2)
+        sim.run_stages(st, spec, "bin", "classify")
+        assert st.particles.count == 64
+        sim.run_stages(st, spec, "reseed", "reseed")
+        assert st.particles.count == 64 * 8 > 64
+        assert int(np.asarray(st.hash.count).sum()) == st.particles.count
+        outs.append([np.array(a) for a in st.particles.arrays()])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)

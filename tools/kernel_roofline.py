@@ -18,7 +18,7 @@ import sys
 N = 24.9e6        # mean particle count entering steps 1..4 after warm-up
 C = 256 ** 3
 FC = 257 * 256 * 256
-R = 3.11e6        # pressure rows
+R = 3.13e6        # pressure rows
 PEAK = 6549.4
 
 # kernel -> (bytes per launch, formula text)
@@ -34,8 +34,12 @@ BYTES = {
     "k_uf_link": (C + 4 * C, "labels + parents"),
     "k_assemble_rows": (8 * 3 * FC / 3 + C + 9 * R, "faces 8F/3 + C + 9R"),
     "k_matvec": (48 * R, "s 8R + diag 8R + nbr 24R + q 8R"),
+    "k_matvec_c": (30 * R, "s 8R + meta 2R + dy 4R + dz 8R + q 8R"),
     "k_dot_nodes<LdProd>": (16 * R, "two vectors"),
     "k_dot_nodes<LdLaneDot>": (28 * R, "zL gather 8R + posL 4R + r 8R + z 8R"),
+    "k_dot_fused<LdProd>": (16 * R, "two vectors"),
+    "k_dot_fused<LdLaneDot>": (28 * R, "zL gather 8R + posL 4R + r 8R + z 8R"),
+    "k_wave_prep": (8 * 256 * 32 * 115, "halo refill: tiles x 32 x nsteps doubles"),
     "k_pcg_update": (60 * R, "x,r r/w 32R + s,q 16R + rL 8R + posL 4R"),
     "k_pcg_dir": (24 * R, "z, s read + s write"),
     "k_mic_cl<0, 4, 4, 4, 3, 0>": (24 * R, "src + precon read, dst write"),
