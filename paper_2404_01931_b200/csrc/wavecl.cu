@@ -32,7 +32,11 @@ namespace {
 
 constexpr int CT = 16;   // tile edge: TY = TZ = 16
 
-constexpr int UH = 4;    // global-halo prefetch depth (steps)
+// global-halo prefetch depth (steps).  Measured at 256^3 (bench, ms/step):
+// UH 1: 72.8, 2: 71.6*, 4: 74.9, 8: 75.9*, no prefetch: 81 (*warm single
+// step).  A consumer runs close behind its producer, so a slot read several
+// steps early is mostly still pending and only adds a wasted global load.
+constexpr int UH = 1;
 
 __device__ __forceinline__ unsigned smem_addr(const void *p) { return smem_u32(p); }
 __device__ __forceinline__ unsigned cluster_rank() {
