@@ -76,16 +76,79 @@ __device__ __forceinline__ double tri_one(const double *__restrict__ arr, int mx
     return c0 * (1.0 - fz) + c1 * fz;
 }
 
+// tri_one on two arrays of the same lattice at the same point (G2P samples
+// grid and grid_old there): the clamping, indices and weights are computed
+// once, each value with tri_one's exact arithmetic.
+__device__ __forceinline__ void tri_pair(const double *__restrict__ a, const double *__restrict__ b,
+                                         int mx, int my, int mz, double gx, double gy, double gz,
+                                         double &va, double &vb) {
+    if (gx < 0.0) gx = 0.0;
+    if (gx > (double)mx - 1.0) gx = (double)mx - 1.0;
+    if (gy < 0.0) gy = 0.0;
+    if (gy > (double)my - 1.0) gy = (double)my - 1.0;
+    if (gz < 0.0) gz = 0.0;
+    if (gz > (double)mz - 1.0) gz = (double)mz - 1.0;
+    int i0 = (int)gx, j0 = (int)gy, k0 = (int)gz;
+    if (i0 > mx - 2) i0 = mx - 2;
+    if (j0 > my - 2) j0 = my - 2;
+    if (k0 > mz - 2) k0 = mz - 2;
+    if (i0 < 0) i0 = 0;
+    if (j0 < 0) j0 = 0;
+    if (k0 < 0) k0 = 0;
+    const double fx = gx - (double)i0, fy = gy - (double)j0, fz = gz - (double)k0;
+    const int i1 = i0 + 1 < mx ? i0 + 1 : mx - 1;
+    const int j1 = j0 + 1 < my ? j0 + 1 : my - 1;
+    const int k1 = k0 + 1 < mz ? k0 + 1 : mz - 1;
+    const int64_t sy = mx, sz = (int64_t)mx * my;
+    const int64_t o[8] = {i0 + j0 * sy + k0 * sz, i1 + j0 * sy + k0 * sz, i0 + j1 * sy + k0 * sz,
+                          i1 + j1 * sy + k0 * sz, i0 + j0 * sy + k1 * sz, i1 + j0 * sy + k1 * sz,
+                          i0 + j1 * sy + k1 * sz, i1 + j1 * sy + k1 * sz};
+    double A[8], B[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        A[q] = __ldg(a + o[q]);
+        B[q] = __ldg(b + o[q]);
+    }
+    const double ex = 1.0 - fx, ey = 1.0 - fy, ez = 1.0 - fz;
+    {
+        const double c00 = A[0] * ex + A[1] * fx, c10 = A[2] * ex + A[3] * fx;
+        const double c01 = A[4] * ex + A[5] * fx, c11 = A[6] * ex + A[7] * fx;
+        const double c0 = c00 * ey + c10 * fy, c1 = c01 * ey + c11 * fy;
+        va = c0 * ez + c1 * fz;
+    }
+    {
+        const double c00 = B[0] * ex + B[1] * fx, c10 = B[2] * ex + B[3] * fx;
+        const double c01 = B[4] * ex + B[5] * fx, c11 = B[6] * ex + B[7] * fx;
+        const double c0 = c00 * ey + c10 * fy, c1 = c01 * ey + c11 * fy;
+        vb = c0 * ez + c1 * fz;
+    }
+}
+
 // flipsim/_kernels/_core.pyx:84-89 — staggered-lattice velocity at a point.
+// (x - origin) / dtau is an exact multiply when dtau = 2^-k (div_dtau).
 __device__ __forceinline__ void sample_vel(const Dims &d, const double *u, const double *v,
                                            const double *w, double px, double py, double pz,
                                            double &vx, double &vy, double &vz) {
-    double gx = (px - d.ox) / d.dtau;
-    double gy = (py - d.oy) / d.dtau;
-    double gz = (pz - d.oz) / d.dtau;
+    double gx = div_dtau(d, px - d.ox);
+    double gy = div_dtau(d, py - d.oy);
+    double gz = div_dtau(d, pz - d.oz);
     vx = tri_one(u, d.nx + 1, d.ny, d.nz, gx, gy - 0.5, gz - 0.5);
     vy = tri_one(v, d.nx, d.ny + 1, d.nz, gx - 0.5, gy, gz - 0.5);
     vz = tri_one(w, d.nx, d.ny, d.nz + 1, gx - 0.5, gy - 0.5, gz);
+}
+
+// sample_vel on the new and old grids at once (G2P, transfer.py:60-82)
+__device__ __forceinline__ void sample_vel_pair(const Dims &d, const double *un, const double *vn,
+                                                const double *wn, const double *uo,
+                                                const double *vo, const double *wo, double px,
+                                                double py, double pz, double &ax, double &ay,
+                                                double &az, double &bx, double &by, double &bz) {
+    const double gx = div_dtau(d, px - d.ox);
+    const double gy = div_dtau(d, py - d.oy);
+    const double gz = div_dtau(d, pz - d.oz);
+    tri_pair(un, uo, d.nx + 1, d.ny, d.nz, gx, gy - 0.5, gz - 0.5, ax, bx);
+    tri_pair(vn, vo, d.nx, d.ny + 1, d.nz, gx - 0.5, gy, gz - 0.5, ay, by);
+    tri_pair(wn, wo, d.nx, d.ny, d.nz + 1, gx - 0.5, gy - 0.5, gz, az, bz);
 }
 
 // flipsim/rng.py:19-33

@@ -171,15 +171,15 @@ __global__ void k_g2p(ParticlePtrs P, int64_t n, Dims d, const double *__restric
     for (int64_t t = gtid(); t < n; t += gstride()) {
         double px = P.a[0][t], py = P.a[1][t], pz = P.a[2][t];
         double ax, ay, az;
-        sample_vel(d, un, vn, wn, px, py, pz, ax, ay, az);
         if (f == 0.0) {
+            sample_vel(d, un, vn, wn, px, py, pz, ax, ay, az);
             P.a[3][t] = ax;
             P.a[4][t] = ay;
             P.a[5][t] = az;
             continue;
         }
         double bx, by, bz;
-        sample_vel(d, uo, vo, wo, px, py, pz, bx, by, bz);
+        sample_vel_pair(d, un, vn, wn, uo, vo, wo, px, py, pz, ax, ay, az, bx, by, bz);
         double g = 1.0 - f;
         P.a[3][t] = g * ax + f * ((P.a[3][t] + ax) - bx);
         P.a[4][t] = g * ay + f * ((P.a[4][t] + ay) - by);
