@@ -44,7 +44,7 @@ extern "C" {
 #define FLIP_E_BREAKDOWN 3   /* SolverBreakdownError (errors.py:25-26) */
 #define FLIP_E_CUDA 4        /* CUDA runtime failure */
 #define FLIP_E_ARG 5         /* bad argument / ValueError */
-#define FLIP_E_CAPACITY 6    /* particle capacity exceeded */
+#define FLIP_E_CAPACITY 6    /* particle count beyond int32 indexing / flip_set_particle_count > capacity */
 
 /* ---- step stages, in reference order (sim.py:233-292) ---- */
 #define FLIP_STAGE_DT 0
@@ -125,9 +125,13 @@ typedef struct {
 const char *flip_last_error(void);
 int flip_device_count(int *count);
 
-/* ctx lifecycle.  capacity <= 0 picks 12 * ncells (the reseed bound,
- * particles.py:152-177).  Grid starts as MacGrid(dims): zero velocities and
- * pressure, every label AIR (grid.py:65-72), no particles. */
+/* ctx lifecycle.  capacity is the initial particle-buffer size; <= 0 picks
+ * 12 * ncells (the reseed bound, particles.py:152-177).  The buffers grow on
+ * demand (flip_set_particles*, flip_seed_regions, the reseed stage), as the
+ * reference's ParticleSet has no capacity; FLIP_E_CAPACITY only reports the
+ * int32 indexing limit (2^31 particles per device).  Grid starts as
+ * MacGrid(dims): zero velocities and pressure, every label AIR
+ * (grid.py:65-72), no particles. */
 int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, double dtau,
                 const double origin[3], int64_t capacity, flip_ctx **out);
 void flip_destroy(flip_ctx *ctx);
@@ -185,8 +189,8 @@ int flip_run_stages(flip_ctx *ctx, const flip_step_params *params, int32_t first
 
 /* Slab decomposition support (multi-GPU, one ctx per GPU; the exchanges run
  * in the host layer over NCCL, paper_2404_01931_b200/dist.py).  Device
- * pointers stay valid until the next stage call (binning and reseed swap the
- * particle buffers). */
+ * pointers stay valid until the next stage or particle setter call (binning
+ * and reseed swap the particle buffers; growth reallocates them). */
 typedef struct {
     double *pos[3], *vel[3];   /* particle SoA, `capacity` entries */
     int32_t *count, *offset;   /* hash: count[ncells], offset[ncells + 1] */
