@@ -868,6 +868,35 @@ __global__ void k_wave_prep(double *halo, int64_t nh, int *ticket, const DevScal
     for (int64_t i = gtid(); i < nh; i += gstride()) halo[i] = m;
 }
 
+// k_wave_prep for the cluster sweep: only tiles that publish across a
+// cluster boundary use the global halo (y: tile rows b % cy == cy - 1 going
+// forward, b % cy == 0 in reverse; z likewise with columns), a quarter of it
+// for 4x4 clusters.  Each selected y row is one contiguous block of the
+// step-major halo_y; each selected z tile one block of halo_z.
+__global__ void k_wave_prep_cl(double *halo_y, double *halo_z, int TB, int TC, int nsteps, int ty,
+                               int tz, int cy, int cz, int rev, int *ticket,
+                               const DevScalars *sc) {
+    if (sc && sc->done) return;
+    if (gtid() == 0) *ticket = 0;
+    const double m = __longlong_as_double((long long)WAVE_PENDING);
+    const int64_t yrow = (int64_t)TC * nsteps * tz;          // one tile row of halo_y
+    const int64_t ny = (int64_t)(TB / cy) * yrow;
+    const int64_t ztile = (int64_t)nsteps * ty;              // one tile of halo_z
+    const int64_t nz = (int64_t)TB * (TC / cz) * ztile;
+    for (int64_t e = gtid(); e < ny + nz; e += gstride()) {
+        if (e < ny) {
+            const int64_t q = e / yrow;
+            const int64_t b = rev ? q * cy : q * cy + cy - 1;
+            halo_y[b * yrow + e % yrow] = m;
+        } else {
+            const int64_t f = e - ny, t = f / ztile;
+            const int64_t b = t / (TC / cz), qc = t % (TC / cz);
+            const int64_t c = rev ? qc * cz : qc * cz + cz - 1;
+            halo_z[(b * TC + c) * ztile + f % ztile] = m;
+        }
+    }
+}
+
 // CF_* flags per cell from the row mask (pressure rows = unpinned FLUID).
 __global__ void k_cell_flags(Dims d, const uint8_t *__restrict__ isrow,
                              unsigned char *__restrict__ cf) {
@@ -1004,7 +1033,21 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
     static const bool v1 = getenv("FLIPB200_LANE_V1") != nullptr;
     const bool lane2 = TY + TZ <= 32 && !v1;  // step-major halo (k_mic_lane2 / k_mic_cl)
     int64_t nh = tiles * (TY + TZ) * (lane2 ? (int64_t)A.geom.nsteps : A.geom.ispan_pad);
-    k_wave_prep<<<nblocks(nh), kThreads, 0, st>>>(A.halo_y, nh, A.ticket, A.sc);
+    static bool cluster_ok = true;
+    int cy = 0, cz = 0;
+    const bool try_cluster = lane2 && TY == 16 && TZ == 16 && cluster_ok &&
+                             mic_cluster_pad(&cy, &cz) && A.geom.TB % cy == 0 &&
+                             A.geom.TC % cz == 0;
+    static const bool full_prep = getenv("FLIPB200_FULL_HALO_PREP") != nullptr;
+    if (try_cluster && !full_prep) {
+        const int64_t nsel = (int64_t)(A.geom.TB / cy) * A.geom.TC * A.geom.nsteps * TZ +
+                             (int64_t)A.geom.TB * (A.geom.TC / cz) * A.geom.nsteps * TY;
+        k_wave_prep_cl<<<nblocks(nsel), kThreads, 0, st>>>(
+            A.halo_y, A.halo_y + tiles * A.geom.nsteps * TZ, A.geom.TB, A.geom.TC, A.geom.nsteps,
+            TY, TZ, cy, cz, REV ? 1 : 0, A.ticket, A.sc);
+    } else {
+        k_wave_prep<<<nblocks(nh), kThreads, 0, st>>>(A.halo_y, nh, A.ticket, A.sc);
+    }
     if constexpr (TY + TZ > 32) {
         k_mic_lane<REV, TY, TZ><<<(unsigned)tiles, TY * TZ, 0, st>>>(A);
     } else {
@@ -1017,7 +1060,6 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
         // DSMEM cluster kernel when its cluster shape can be scheduled here;
         // otherwise (e.g. no 16-CTA clusters on this device) k_mic_lane2 for
         // the rest of the process: same arithmetic, same padded tile grid
-        static bool cluster_ok = true;
         if (TY == 16 && TZ == 16 && cluster_ok) {
             cudaError_t e = launch_mic_cluster(REV, B, st);
             if (e == cudaSuccess) return e;
@@ -1028,6 +1070,9 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
                         cudaGetErrorString(e));
             }
         }
+        // k_mic_lane2 reads every tile's halo: the whole of it after a selective prep
+        if (try_cluster && !full_prep)
+            k_wave_prep<<<nblocks(nh), kThreads, 0, st>>>(A.halo_y, nh, A.ticket, A.sc);
         if (lane_chunk() > 0) {
             constexpr int KC = 8;
             constexpr int smem = LANE_NB * 2 * KC * TY * TZ * 8;
