@@ -156,3 +156,41 @@ def test_energy_matches_oracle_pairwise(pkg):
     e_ref = (0.5 * float(np.add.reduce(P[3] ** 2 + P[4] ** 2 + P[5] ** 2))
              + g * float(np.add.reduce(P[1] - floor)))
     assert e_dev == e_ref
+
+
+@pytest.mark.parametrize("case", [dict(name="dam-break", res=128, solver="pcg"),
+                                  dict(name="double-dam-break-obstacle", res=96, solver="pcg")],
+                         ids=["dam-break-128", "double-dam-break-obstacle-96"])
+def test_multicluster_sweep_bit_exact(pkg, case):
+    """The MIC(0) sweep with more than one 4x4 cluster of 16x16 tiles (rows
+    spanning > 64 cells in y or z): tile faces then also cross clusters
+    through the global halo (helper polls, selective halo prep), a path the
+    small cases above never reach."""
+    dspec, ospec = spec_pair(**case)
+    st = pkg.make_scene(dspec, rng_seed=1)
+    os_ = O.make_scene(ospec, rng_seed=1)
+    lab = np.asarray(st.grid.label).reshape(case["res"], case["res"], case["res"])
+    k, j, _ = np.nonzero(lab == pkg.FLUID)
+    assert max(np.ptp(j), np.ptp(k)) + 1 > 64
+    for step in range(2):
+        rep = pkg.step(st, dspec)
+        ref = O.step(os_, ospec)
+        bad = diff_report(device_arrays(st), oracle_arrays(os_))
+        assert not bad, f"step {step}: {bad}"
+        assert rep.solver_iterations == ref["solver_iterations"]
+        assert rep.solver_residual == ref["solver_residual"]
+
+
+def test_full_size_step_bit_exact(pkg):
+    """BASELINE's full size: the 256^3 dam-break (24.7M particles) make_scene
+    and one step, every byte equal to the oracle's."""
+    dspec, ospec = spec_pair(name="dam-break", res=256, solver="pcg")
+    st = pkg.make_scene(dspec, rng_seed=0)
+    os_ = O.make_scene(ospec, rng_seed=0)
+    assert st.particles.count == os_.parts[0].size > 24_000_000
+    rep = pkg.step(st, dspec)
+    ref = O.step(os_, ospec)
+    bad = diff_report(device_arrays(st), oracle_arrays(os_))
+    assert not bad, f"256^3 step: {bad}"
+    assert rep.solver_iterations == ref["solver_iterations"]
+    assert rep.solver_residual == ref["solver_residual"]
