@@ -1393,7 +1393,6 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         LB.args.trace = getenv("FLIPB200_WAVE_TRACE") ? c.wave_trace : nullptr;
         if (LB.args.trace) cudaMemsetAsync(c.wave_trace, 0, 8 * 32768, st);  // (trace buffer: 32768 u64)
         LB.args.dbg = getenv("FLIPB200_LANE_DBG") ? atoi(getenv("FLIPB200_LANE_DBG")) : 0;
-        LB.args.mode = getenv("FLIPB200_LANE_MODE") ? atoi(getenv("FLIPB200_LANE_MODE")) : 0;
         LB.posL = c.posL;
         LB.rL = c.laneA;
         LB.tqL = c.laneB;

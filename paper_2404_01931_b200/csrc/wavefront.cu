@@ -535,24 +535,22 @@ __global__ void __launch_bounds__(TY *TZ) k_mic_lane(LaneArgs A) {
         for (int u = 0; u < U; u++) {
             const int s = s0 + u;
             if (s >= nsteps) break;  // uniform
-            if (!(A.dbg & 1)) __syncthreads();
+            __syncthreads();
             if (A.trace && tile == 0 && p == 0 && s < 256) A.trace[s] = (unsigned long long)clock64();
             const int cur = s & 1, prv = cur ^ 1;
-            const double a = (A.dbg & 4) ? 1.0 : av[u], pr = (A.dbg & 4) ? 1.0 : bv[u];
+            const double a = av[u], pr = bv[u];
             const int x = xof(s);
             double out = absent;
             if (present(a) && valid && x >= 0 && x < G.ispan) {
                 double yv = absent, zv = absent;
-                if (A.dbg & 8) {
-                } else if (y_local) {
+                if (y_local) {
                     yv = sval[prv][kk][yj];
                 } else if (hy_in) {
                     cp_async_wait<U - 1>();
                     yv = hyb[kk][x % HR];
                     if (is_pending(yv)) yv = poll_ready(hy_in + x);
                 }
-                if (A.dbg & 8) {
-                } else if (z_local) {
+                if (z_local) {
                     zv = sval[prv][zk][jj];
                 } else if (hz_in) {
                     cp_async_wait<U - 1>();
@@ -565,7 +563,7 @@ __global__ void __launch_bounds__(TY *TZ) k_mic_lane(LaneArgs A) {
                     if (present(yv)) t += yv;
                     if (present(zv)) t += zv;
                     double q = t * pr;
-                    if (!(A.dbg & 32)) dstL[(int64_t)lstep(s) * TP] = q;
+                    dstL[(int64_t)lstep(s) * TP] = q;
                     out = (sc * pr) * q;
                 } else {  // _core.pyx:333-346
                     double t = a;
@@ -574,16 +572,16 @@ __global__ void __launch_bounds__(TY *TZ) k_mic_lane(LaneArgs A) {
                     if (present(yv)) t += sp * yv;
                     if (present(zv)) t += sp * zv;
                     out = t * pr;
-                    if (!(A.dbg & 32)) dstL[(int64_t)lstep(s) * TP] = out;
+                    dstL[(int64_t)lstep(s) * TP] = out;
                 }
             }
             sval[cur][kk][jj] = out;
             pv = out;
-            if (!(A.dbg & 2) && (hy_out || hz_out) && valid && x >= 0 && x < G.ispan) {
+            if ((hy_out || hz_out) && valid && x >= 0 && x < G.ispan) {
                 if (hy_out) publish(hy_out + x, out);
                 if (hz_out) publish(hz_out + x, out);
             }
-            if (!(A.dbg & 16)) load(s + U, u);
+            load(s + U, u);
         }
     }
     cp_async_wait<0>();

@@ -157,8 +157,7 @@ struct LaneArgs {
     int *ticket;
     const DevScalars *sc;
     unsigned long long *trace;  // optional per-step clock of tile 0 lane 0
-    int dbg;                    // ablation bits (timing experiments only)
-    int mode;                   // helper halo policy bits (FLIPB200_LANE_MODE)
+    int dbg;                    // traced tile index (FLIPB200_LANE_DBG, with FLIPB200_WAVE_TRACE)
 };
 
 cudaError_t launch_wave(int mode, const WaveArgs &A, cudaStream_t st);
