@@ -14,10 +14,12 @@ the reference's own scene builder restated on the device (synthetic, seed 0).
 * e2e       the same metric through the C ABI with HOST buffers: every step
             uploads particles + labels from pinned host memory, steps, and
             downloads the particles.
-* roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_lane2,
-            forward + backward, ~55% of the step): algorithmic bytes (3 x 8 B
+* roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_cl,
+            forward + backward, ~56% of the step): algorithmic bytes (3 x 8 B
             per row) over the measured per-launch time (CUDA events
             bracketing each launch on the library's stream).
+* clocks    nvidia-smi every 50 ms from before the warm-up; only samples
+            inside the timed region's wall-clock window are kept.
 * cpu_baseline  the oracle (C restatement of the reference step, all host
             threads) on a bounded sample of the same workload.
 * --impl reference  times the oracle port as the reference arm (the Python
@@ -34,6 +36,7 @@ scene ("scaling": "strong"); results are bit-identical to one GPU.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -81,7 +84,7 @@ def workload(args) -> dict:
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -89,14 +92,21 @@ class ClockSampler:
         self.idx = gpu_index
         self.proc = None
         self.path = f"/tmp/flipb200_clocks_{os.getpid()}.csv"
+        self.window = None
 
     def start(self):
+        """Started before the warm-up (nvidia-smi takes a while to begin
+        sampling); mark() brackets the timed region and only samples inside
+        it are kept."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
-                 "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -106,18 +116,23 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 7 or f[0] != str(self.idx):
+            if len(f) < 8 or f[1] != str(self.idx):
                 continue
             try:
-                sm.append(float(f[1]))
-                mx.append(float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]), f[4:8]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[3:7]):
+        if self.window is not None:
+            inside = [r for r in rows if self.window[0] <= r[0] <= self.window[1]]
+            rows = inside or sorted(rows, key=lambda r: abs(r[0] - self.window[1]))[:1]
+        sm, mx, reasons = [r[1] for r in rows], [r[2] for r in rows], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None,
@@ -222,6 +237,8 @@ def run_ours(args):
         do_step = P.step
     dev = st.device
     n0 = st.particles.count
+    clocks = ClockSampler(local)
+    clocks.start()
     warm = max(3, args.warmup)
     for _ in range(warm):
         do_step(st, spec)
@@ -232,11 +249,10 @@ def run_ours(args):
             dist.barrier()
 
     # ---------------- device-resident timed region ----------------
-    clocks = ClockSampler(local)
     check(LIB.flip_set_probe(dev.ctx, 1))
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    wall0 = time.time()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -257,6 +273,7 @@ def run_ours(args):
     e1.synchronize()
     torch.cuda.synchronize()
     barrier()
+    clocks.mark(wall0, time.time())
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     pms, plaunch, pbytes = C.c_double(0), C.c_int64(0), C.c_double(0)
