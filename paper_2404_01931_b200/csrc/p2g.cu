@@ -62,15 +62,17 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
       const uint8_t *__restrict__ label, const DevScalars *__restrict__ sc, double g,
       int fuse_force) {
     FaceLattice L = lattice(d, comp);
-    int64_t nf = (int64_t)L.fnx * L.fny * L.fnz;
+    // 32-bit index math: flip_create rejects grids with >= 2^31 faces
+    const unsigned nf = (unsigned)L.fnx * L.fny * L.fnz;
     int nx = d.nx, ny = d.ny, nz = d.nz;
-    int64_t sxy = (int64_t)nx * ny;
+    const int sxy = nx * ny;
     double gdt = 0.0;
     if (fuse_force && g != 0.0) gdt = g * sc->dt;
-    for (int64_t f = gtid(); f < nf; f += gstride()) {
-        int fi = (int)(f % L.fnx);
-        int fj = (int)((f / L.fnx) % L.fny);
-        int fk = (int)(f / ((int64_t)L.fnx * L.fny));
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
+        const unsigned fq = f / (unsigned)L.fnx;
+        int fi = (int)(f - fq * (unsigned)L.fnx);
+        int fj = (int)(fq % (unsigned)L.fny);
+        int fk = (int)(fq / (unsigned)L.fny);
         double fpx = d.ox + ((double)fi + L.offx) * d.dtau;
         double fpy = d.oy + ((double)fj + L.offy) * d.dtau;
         double fpz = d.oz + ((double)fk + L.offz) * d.dtau;
@@ -80,7 +82,7 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
         double num = 0.0, dsum = 0.0, cn = 0.0, cd = 0.0;
         for (int cz = czlo; cz <= czhi; cz++) {
             for (int cy = cylo; cy <= cyhi; cy++) {
-                int64_t row = (int64_t)cy * nx + cz * sxy;
+                const int row = cy * nx + cz * sxy;
                 int nseg = CONTIG ? 1 : cxhi - cxlo + 1;
                 for (int sgi = 0; sgi < nseg; sgi++) {
                     int t0, t1;
@@ -88,7 +90,7 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
                         t0 = __ldg(offset + row + cxlo);
                         t1 = __ldg(offset + row + cxhi + 1);
                     } else {
-                        int64_t cell = row + cxlo + sgi;
+                        const int cell = row + cxlo + sgi;
                         t0 = __ldg(offset + cell);
                         t1 = t0 + __ldg(count + cell);
                     }
