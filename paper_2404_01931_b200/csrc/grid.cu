@@ -14,6 +14,18 @@ __host__ __device__ inline Lat lat(const Dims &d, int comp) {
     return {d.nx, d.ny, d.nz + 1};
 }
 
+// (i, j, k) of face f with 32-bit unsigned division (face counts are below
+// 2^31, checked by flip_create): two divides instead of three 64-bit ones.
+__device__ __forceinline__ void lat_ijk(const Lat &L, unsigned f, int &i, int &j, int &k) {
+    const unsigned q = f / (unsigned)L.mx;
+    i = (int)(f - q * (unsigned)L.mx);
+    const unsigned r = q / (unsigned)L.my;
+    j = (int)(q - r * (unsigned)L.my);
+    k = (int)r;
+}
+__device__ __forceinline__ unsigned ugtid() { return blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ unsigned ugstride() { return gridDim.x * blockDim.x; }
+
 // Low/high cell of an interior face along its component axis; false on the
 // domain boundary.
 __device__ __forceinline__ bool face_cells(const Dims &d, int comp, int i, int j, int k,
@@ -39,10 +51,11 @@ __global__ void k_force_enforce(double *__restrict__ a, Dims d, int comp, double
                                 const DevScalars *__restrict__ sc, int apply_force,
                                 const uint8_t *__restrict__ label) {
     Lat L = lat(d, comp);
-    int64_t n = (int64_t)L.mx * L.my * L.mz;
+    const unsigned n = (unsigned)L.mx * L.my * L.mz;
     double inc = (apply_force && g != 0.0) ? g * sc->dt : 0.0;
-    for (int64_t f = gtid(); f < n; f += gstride()) {
-        int i = (int)(f % L.mx), j = (int)((f / L.mx) % L.my), k = (int)(f / ((int64_t)L.mx * L.my));
+    for (unsigned f = ugtid(); f < n; f += ugstride()) {
+        int i, j, k;
+        lat_ijk(L, f, i, j, k);
         int64_t lo, hi;
         bool solid = !face_cells(d, comp, i, j, k, lo, hi) || label[lo] == SOLID || label[hi] == SOLID;
         if (solid) a[f] = 0.0;
@@ -76,10 +89,11 @@ __global__ void k_gradient(double *__restrict__ a, Dims d, int comp, const doubl
                            const uint8_t *__restrict__ label, const DevScalars *__restrict__ sc,
                            double rho_dtau) {
     Lat L = lat(d, comp);
-    int64_t n = (int64_t)L.mx * L.my * L.mz;
+    const unsigned n = (unsigned)L.mx * L.my * L.mz;
     double scale = sc->dt / rho_dtau;
-    for (int64_t f = gtid(); f < n; f += gstride()) {
-        int i = (int)(f % L.mx), j = (int)((f / L.mx) % L.my), k = (int)(f / ((int64_t)L.mx * L.my));
+    for (unsigned f = ugtid(); f < n; f += ugstride()) {
+        int i, j, k;
+        lat_ijk(L, f, i, j, k);
         int64_t lo, hi;
         if (!face_cells(d, comp, i, j, k, lo, hi)) {
             a[f] = 0.0;
@@ -97,13 +111,15 @@ __global__ void k_gradient(double *__restrict__ a, Dims d, int comp, const doubl
 // Accumulation order: 0 + v(k+1) + v(k-1) + v(j+1) + v(j-1) + v(i+1) + v(i-1).
 __global__ void k_extrap_layer(double *__restrict__ A, double *__restrict__ B, Lat L,
                                const uint8_t *__restrict__ kin, uint8_t *__restrict__ kout) {
-    int64_t n = (int64_t)L.mx * L.my * L.mz, sy = L.mx, sz = (int64_t)L.mx * L.my;
-    for (int64_t f = gtid(); f < n; f += gstride()) {
+    const unsigned n = (unsigned)L.mx * L.my * L.mz;
+    const int64_t sy = L.mx, sz = (int64_t)L.mx * L.my;
+    for (unsigned f = ugtid(); f < n; f += ugstride()) {
         if (kin[f]) {
             kout[f] = 1;
             continue;
         }
-        int i = (int)(f % L.mx), j = (int)((f / L.mx) % L.my), k = (int)(f / sz);
+        int i, j, k;
+        lat_ijk(L, f, i, j, k);
         int64_t nb[6] = {f + sz, f - sz, f + sy, f - sy, f + 1, f - 1};
         bool ok[6] = {k + 1 < L.mz, k >= 1, j + 1 < L.my, j >= 1, i + 1 < L.mx, i >= 1};
         double a = 0.0, b = 0.0;
