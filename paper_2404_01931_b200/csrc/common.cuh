@@ -39,6 +39,16 @@ __device__ __forceinline__ double div_dtau(const Dims &d, double x) {
     return d.pow2 ? x * d.inv_dtau : x / d.dtau;
 }
 
+// (i, j, k) of cell c with 32-bit unsigned division (cell counts are below
+// 2^31, checked by flip_create).
+__device__ __forceinline__ void cell_ijk(const Dims &d, int64_t c, int &i, int &j, int &k) {
+    const unsigned u = (unsigned)c, q = u / (unsigned)d.nx;
+    i = (int)(u - q * (unsigned)d.nx);
+    const unsigned r = q / (unsigned)d.ny;
+    j = (int)(q - r * (unsigned)d.ny);
+    k = (int)r;
+}
+
 // flipsim/_kernels/_core.pyx:17-19
 __device__ __forceinline__ double hat(double r) {
     r = fabs(r);

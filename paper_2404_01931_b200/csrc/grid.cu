@@ -172,7 +172,8 @@ __global__ void k_divergence(Dims d, const double *__restrict__ u, const double 
                              const double *__restrict__ w, double *__restrict__ div) {
     int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
     for (int64_t c = gtid(); c < nc; c += gstride()) {
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         int64_t fu = i + (int64_t)j * (d.nx + 1) + k * (int64_t)(d.nx + 1) * d.ny;
         int64_t fv = i + (int64_t)j * d.nx + k * (int64_t)d.nx * (d.ny + 1);
         int64_t fw = c;

@@ -53,7 +53,8 @@ __global__ void k_box_reduce(const uint8_t *__restrict__ label, Dims d, DevScala
     int mn[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, mx[3] = {-1, -1, -1};
     for (int64_t c = gtid(); c < nc; c += gstride()) {
         if (label[c] == SOLID) continue;
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((int64_t)d.nx * d.ny));
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         mn[0] = min(mn[0], i); mx[0] = max(mx[0], i);
         mn[1] = min(mn[1], j); mx[1] = max(mx[1], j);
         mn[2] = min(mn[2], k); mx[2] = max(mx[2], k);
@@ -355,7 +356,8 @@ int stage_reseed(Ctx &c, const flip_step_params &prm) {
 __global__ void k_solid_shell(uint8_t *label, Dims d) {
     int64_t nc = d.ncells();
     for (int64_t c = gtid(); c < nc; c += gstride()) {
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((int64_t)d.nx * d.ny));
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         if (i == 0 || j == 0 || k == 0 || i == d.nx - 1 || j == d.ny - 1 || k == d.nz - 1)
             label[c] = SOLID;
     }
@@ -364,7 +366,8 @@ __global__ void k_solid_shell(uint8_t *label, Dims d) {
 __global__ void k_solid_box(uint8_t *label, Dims d, int i0, int i1, int j0, int j1, int k0, int k1) {
     int64_t nc = d.ncells();
     for (int64_t c = gtid(); c < nc; c += gstride()) {
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / ((int64_t)d.nx * d.ny));
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         if (i >= i0 && i <= i1 && j >= j0 && j <= j1 && k >= k0 && k <= k1) label[c] = SOLID;
     }
 }

@@ -115,7 +115,8 @@ __global__ void k_uf_link_runs(const uint8_t *__restrict__ label, Dims d, int *p
     int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
     for (int64_t c = gtid(); c < nc; c += gstride()) {
         if (label[c] != FLUID) continue;
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         const bool wfl = i > 0 && label[c - 1] == FLUID;
         if (j > 0 && label[c - d.nx] == FLUID && !(wfl && label[c - 1 - d.nx] == FLUID))
             uf_unite(par, (int)c, (int)(c - d.nx));
@@ -128,7 +129,8 @@ __global__ void k_uf_link(const uint8_t *__restrict__ label, Dims d, int *par) {
     int64_t nc = d.ncells(), sxy = (int64_t)d.nx * d.ny;
     for (int64_t c = gtid(); c < nc; c += gstride()) {
         if (label[c] != FLUID) continue;
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         if (i > 0 && label[c - 1] == FLUID) uf_unite(par, (int)c, (int)(c - 1));
         if (j > 0 && label[c - d.nx] == FLUID) uf_unite(par, (int)c, (int)(c - d.nx));
         if (k > 0 && label[c - sxy] == FLUID) uf_unite(par, (int)c, (int)(c - sxy));
@@ -146,7 +148,8 @@ __global__ void k_uf_finish(const uint8_t *__restrict__ label, Dims d, int *par,
         if (label[c] != FLUID) continue;
         int root = uf_rep((volatile int *)par, (int)c);
         par[c] = root;
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         bool air = lab_at(label, d, i - 1, j, k) == AIR || lab_at(label, d, i + 1, j, k) == AIR ||
                    lab_at(label, d, i, j - 1, k) == AIR || lab_at(label, d, i, j + 1, k) == AIR ||
                    lab_at(label, d, i, j, k - 1) == AIR || lab_at(label, d, i, j, k + 1) == AIR;
@@ -194,7 +197,8 @@ __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
     int lo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, hi[3] = {-1, -1, -1};
     for (int64_t r = gtid(); r < n; r += gstride()) {
         int64_t c = cell_of_row[r];
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sxy);
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0}, dk[6] = {0, 0, 0, 0, -1, 1};
         int ns = 0;
         uint8_t nl[6];

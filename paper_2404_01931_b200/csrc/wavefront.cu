@@ -827,10 +827,12 @@ __global__ void k_lane_map(WaveGeom G, Dims d, int TY, int TZ, const uint8_t *__
     const int TP = TY * TZ;
     const double ab = __longlong_as_double((long long)WAVE_ABSENT);
     for (int64_t e = gtid(); e < nL; e += gstride()) {
-        int p = (int)(e % TP);
-        int64_t ts = e / TP;
-        int s = (int)(ts % G.nsteps);
-        int tile = (int)(ts / G.nsteps);
+        // 32-bit decomposition: lane entries stay below 2^31 (lane_entries_max)
+        const unsigned ue = (unsigned)e, ts = ue / (unsigned)TP;
+        int p = (int)(ue - ts * (unsigned)TP);
+        const unsigned tq = ts / (unsigned)G.nsteps;
+        int s = (int)(ts - tq * (unsigned)G.nsteps);
+        int tile = (int)tq;
         int b = tile / G.TC, c = tile % G.TC;
         int jj = p % TY, kk = p / TY;
         int i = G.ilo + s - jj - kk, j = G.jlo + b * TY + jj, k = G.klo + c * TZ + kk;
@@ -900,7 +902,8 @@ __global__ void k_cell_flags(Dims d, const uint8_t *__restrict__ isrow,
                              unsigned char *__restrict__ cf) {
     int64_t nc = d.ncells(), sy = d.nx, sz = (int64_t)d.nx * d.ny;
     for (int64_t c = gtid(); c < nc; c += gstride()) {
-        int i = (int)(c % d.nx), j = (int)((c / d.nx) % d.ny), k = (int)(c / sz);
+        int i, j, k;
+        cell_ijk(d, c, i, j, k);
         unsigned char f = 0;
         if (isrow[c]) {
             f = CF_ROW;
