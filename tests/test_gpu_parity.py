@@ -194,3 +194,19 @@ def test_full_size_step_bit_exact(pkg):
     assert not bad, f"256^3 step: {bad}"
     assert rep.solver_iterations == ref["solver_iterations"]
     assert rep.solver_residual == ref["solver_residual"]
+
+
+def test_config2_jacobi_128_bit_exact(pkg):
+    """BASELINE config 2: dam-break 128^3 with solver="jacobi" (cap 2000),
+    make_scene and one step, every byte equal to the oracle's."""
+    dspec, ospec = spec_pair(name="dam-break", res=128, solver="jacobi")
+    st = pkg.make_scene(dspec, rng_seed=0)
+    os_ = O.make_scene(ospec, rng_seed=0)
+    assert st.particles.count == 3_032_064
+    rep = pkg.step(st, dspec)
+    ref = O.step(os_, ospec)
+    bad = diff_report(device_arrays(st), oracle_arrays(os_))
+    assert not bad, f"128^3 jacobi step: {bad}"
+    assert rep.solver_iterations == ref["solver_iterations"]
+    assert rep.solver_residual == ref["solver_residual"]
+    assert rep.solver_converged == ref["solver_converged"]
