@@ -210,3 +210,19 @@ def test_config2_jacobi_128_bit_exact(pkg):
     assert rep.solver_iterations == ref["solver_iterations"]
     assert rep.solver_residual == ref["solver_residual"]
     assert rep.solver_converged == ref["solver_converged"]
+
+
+def test_config1_64_hundred_steps_bit_exact(pkg):
+    """BASELINE config 1 (`flipsim run --res 64 --steps 100`): 100 steps of
+    the 64^3 dam-break, state compared every 10 steps -- no drift."""
+    dspec, ospec = spec_pair(name="dam-break", res=64, solver="pcg")
+    st = pkg.make_scene(dspec, rng_seed=0)
+    os_ = O.make_scene(ospec, rng_seed=0)
+    assert st.particles.count == 365_056
+    for k in range(100):
+        rep = pkg.step(st, dspec)
+        ref = O.step(os_, ospec)
+        assert rep.solver_iterations == ref["solver_iterations"], k
+        if k % 10 == 9:
+            bad = diff_report(device_arrays(st), oracle_arrays(os_))
+            assert not bad, f"step {k}: {bad}"
