@@ -17,6 +17,8 @@ CASES = [
     dict(spec=dict(name="dam-break", res=16, solver="pcg"), seed=3, steps=3),
     dict(spec=dict(name="double-dam-break", res=20, solver="jacobi"), seed=1, steps=2),
     dict(spec=dict(name="water-drop", res=16, solver="pcg"), seed=2, steps=3),
+    # larger: several clusters in the sweep, heavy slab-crossing migration
+    dict(spec=dict(name="dam-break", res=64, solver="pcg"), seed=0, steps=4),
 ]
 
 
