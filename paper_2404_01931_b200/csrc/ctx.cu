@@ -324,6 +324,7 @@ extern "C" int flip_set_grid(flip_ctx *c, const double *u, const double *v, cons
     TRY(h2d(c->w, w, sizeof(double) * c->nfw, c->st));
     TRY(h2d(c->p, p, sizeof(double) * c->ncells, c->st));
     TRY(h2d(c->label, label, c->ncells, c->st));
+    c->box_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -551,6 +552,7 @@ extern "C" int flip_get_known(flip_ctx *c, uint8_t *ku, uint8_t *kv, uint8_t *kw
 extern "C" int flip_set_solid_shell(flip_ctx *c) {
     cudaSetDevice(c->device);
     launch_set_solid_shell(*c);
+    c->box_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -568,6 +570,7 @@ extern "C" int flip_set_solid_box(flip_ctx *c, int64_t i0, int64_t i1, int64_t j
         b[2 * a + 1] = (int)hi[a];
     }
     launch_set_solid_box(*c, b);
+    c->box_valid = 0;
     return flip_synchronize(c);
 }
 

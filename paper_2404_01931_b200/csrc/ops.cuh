@@ -53,6 +53,7 @@ struct Ctx {
     int64_t slab_c0 = 0, slab_c1 = -1;  // reseed cell range (flip_set_slab); -1: all
     void *f32_buf = nullptr;           // snapshot staging (flip_*_particles_f32)
     void *mg = nullptr;                // multigrid levels (mg.cu), allocated on first use
+    int box_valid = 0;                 // sc->lo/hi hold interior_box of the current SOLID cells
     unsigned short *nb_meta = nullptr; // compact PCG stencil (k_compact_nbr), nc entries
     unsigned *nb_dy = nullptr;
     int2 *nb_dz = nullptr;

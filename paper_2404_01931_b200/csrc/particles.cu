@@ -102,11 +102,16 @@ __global__ void k_advect_key(ParticlePtrs P, int64_t n, const DevScalars *__rest
 }
 
 void stage_advect(Ctx &c, const flip_step_params &prm) {
-    k_box_reset<<<1, 1, 0, c.st>>>(c.sc);
-    k_box_reduce<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.d, c.sc);
-    k_box_final<<<1, 1, 0, c.st>>>(c.d, c.sc);
+    // interior_box (grid.py:121-132) depends only on the SOLID cells, which no
+    // stage changes: recomputed after a label setter invalidated it
+    if (!c.box_valid) {
+        k_box_reset<<<1, 1, 0, c.st>>>(c.sc);
+        k_box_reduce<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.d, c.sc);
+        k_box_final<<<1, 1, 0, c.st>>>(c.d, c.sc);
+        c.launches += 3;
+        c.box_valid = 1;
+    }
     cudaMemsetAsync(c.count, 0, sizeof(int) * c.ncells, c.st);
-    c.launches += 3;
     if (c.n > 0) {
         k_advect_key<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.sc, prm.skin_h, c.d, c.keys0,
                                                           c.count);
