@@ -147,7 +147,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
                     c->has_air, c->cell_of_row, c->nbr, c->diagd, c->rhs, c->x, c->r, c->z, c->s,
                     c->q, c->tq, c->precon, c->xtmp, c->u64_scratch, c->lvl, c->lvl_rows,
-                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->lrow, c->posL, c->laneA, c->laneB, c->laneC, c->laneD, c->sc, c->f32_buf, c->nb_meta, c->nb_dy, c->nb_dz};
+                    c->lvl_off, c->lvl_cnt, c->dot_part, c->wave_prog, c->wave_halo, c->cflags, c->wave_trace, c->lrow, c->posL, c->laneA, c->laneB, c->laneC, c->laneD, c->sc, c->f32_buf, c->nb_meta, c->nb_dy, c->nb_dz, c->solid_list};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
@@ -325,6 +325,7 @@ extern "C" int flip_set_grid(flip_ctx *c, const double *u, const double *v, cons
     TRY(h2d(c->p, p, sizeof(double) * c->ncells, c->st));
     TRY(h2d(c->label, label, c->ncells, c->st));
     c->box_valid = 0;
+    c->faces_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -553,6 +554,7 @@ extern "C" int flip_set_solid_shell(flip_ctx *c) {
     cudaSetDevice(c->device);
     launch_set_solid_shell(*c);
     c->box_valid = 0;
+    c->faces_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -571,6 +573,7 @@ extern "C" int flip_set_solid_box(flip_ctx *c, int64_t i0, int64_t i1, int64_t j
     }
     launch_set_solid_box(*c, b);
     c->box_valid = 0;
+    c->faces_valid = 0;
     return flip_synchronize(c);
 }
 

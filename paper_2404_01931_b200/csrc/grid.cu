@@ -74,7 +74,73 @@ void stage_force(Ctx &c, const flip_step_params &prm) {
     }
 }
 
+// Faces that enforce_solid_boundaries zeroes (domain boundary or next to a
+// SOLID cell): static while no label setter runs, so they are listed once
+// (order irrelevant) and the per-step enforcement is a scatter of zeros.
+__global__ void k_solid_faces(Dims d, int comp, const uint8_t *__restrict__ label,
+                              int *__restrict__ list, unsigned long long *cnt) {
+    Lat L = lat(d, comp);
+    const unsigned n = (unsigned)L.mx * L.my * L.mz;
+    for (unsigned f = ugtid(); f < n; f += ugstride()) {
+        int i, j, k;
+        lat_ijk(L, f, i, j, k);
+        int64_t lo, hi;
+        if (!face_cells(d, comp, i, j, k, lo, hi) || label[lo] == SOLID || label[hi] == SOLID) {
+            const unsigned long long q = atomicAdd(cnt, 1ull);
+            if (list) list[q] = (int)f;
+        }
+    }
+}
+
+__global__ void k_zero_list(double *__restrict__ a, const int *__restrict__ list, int64_t n) {
+    for (int64_t t = gtid(); t < n; t += gstride()) a[list[t]] = 0.0;
+}
+
+static int build_solid_lists(Ctx &c) {
+    unsigned long long cnt[3];
+    FLIP_CUDA_OK(cudaMemsetAsync(c.u64_scratch, 0, 3 * sizeof(unsigned long long), c.st));
+    for (int comp = 0; comp < 3; comp++) {
+        Lat L = lat(c.d, comp);
+        k_solid_faces<<<nblocks((int64_t)L.mx * L.my * L.mz), kThreads, 0, c.st>>>(
+            c.d, comp, c.label, nullptr, c.u64_scratch + comp);
+    }
+    FLIP_CUDA_OK(cudaMemcpyAsync(cnt, c.u64_scratch, sizeof(cnt), cudaMemcpyDeviceToHost, c.st));
+    FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
+    const int64_t total = (int64_t)(cnt[0] + cnt[1] + cnt[2]);
+    if (total > c.solid_cap) {
+        cudaFree(c.solid_list);
+        c.solid_list = nullptr;
+        c.solid_cap = 0;
+        FLIP_CUDA_OK(cudaMalloc(&c.solid_list, sizeof(int) * (size_t)(total > 0 ? total : 1)));
+        c.solid_cap = total;
+    }
+    FLIP_CUDA_OK(cudaMemsetAsync(c.u64_scratch, 0, 3 * sizeof(unsigned long long), c.st));
+    int64_t off = 0;
+    for (int comp = 0; comp < 3; comp++) {
+        Lat L = lat(c.d, comp);
+        k_solid_faces<<<nblocks((int64_t)L.mx * L.my * L.mz), kThreads, 0, c.st>>>(
+            c.d, comp, c.label, c.solid_list + off, c.u64_scratch + comp);
+        c.solid_off[comp] = off;
+        c.solid_cnt[comp] = (int64_t)cnt[comp];
+        off += (int64_t)cnt[comp];
+    }
+    c.launches += 6;
+    c.faces_valid = 1;
+    return 0;
+}
+
 void launch_enforce(Ctx &c, double *u, double *v, double *w) {
+    if (!c.faces_valid && build_solid_lists(c) != 0) cudaGetLastError();  // else: full pass
+    if (c.faces_valid) {
+        double *arr[3] = {u, v, w};
+        for (int comp = 0; comp < 3; comp++) {
+            if (c.solid_cnt[comp] == 0) continue;
+            k_zero_list<<<nblocks(c.solid_cnt[comp]), kThreads, 0, c.st>>>(
+                arr[comp], c.solid_list + c.solid_off[comp], c.solid_cnt[comp]);
+            c.launches++;
+        }
+        return;
+    }
     double *arr[3] = {u, v, w};
     int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
     for (int comp = 0; comp < 3; comp++) {

@@ -54,6 +54,9 @@ struct Ctx {
     void *f32_buf = nullptr;           // snapshot staging (flip_*_particles_f32)
     void *mg = nullptr;                // multigrid levels (mg.cu), allocated on first use
     int box_valid = 0;                 // sc->lo/hi hold interior_box of the current SOLID cells
+    int faces_valid = 0;               // solid_list holds the faces enforce_solid_boundaries zeroes
+    int *solid_list = nullptr;
+    int64_t solid_cap = 0, solid_off[3] = {0, 0, 0}, solid_cnt[3] = {0, 0, 0};
     unsigned short *nb_meta = nullptr; // compact PCG stencil (k_compact_nbr), nc entries
     unsigned *nb_dy = nullptr;
     int2 *nb_dz = nullptr;
