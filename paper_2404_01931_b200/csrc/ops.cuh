@@ -153,6 +153,28 @@ int64_t dot_tmp_doubles(int64_t n);
 void launch_pairwise_dot(const double *a, const double *b, int64_t n, double *tmp,
                          double *out_dev, cudaStream_t st, int64_t *launches);
 
+// Programmatic dependent launch: kernels launched with launch_pdl may be
+// scheduled while their predecessor on the stream drains; they execute
+// pdl_wait() before touching anything it wrote (a no-op without the launch
+// attribute, so the same kernels stay safe from any other call site).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                       cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 inline unsigned nblocks(int64_t n, int threads = kThreads, int64_t cap = 148 * 32) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;

@@ -425,6 +425,7 @@ template <class LD>
 __global__ void __launch_bounds__(256, kDotBlocksPerSM)
 k_dot_fused(LD ld, int64_t n, int cut, double *__restrict__ part, unsigned *ticket, int epi,
             DevScalars *sc, double *final_out, int skip_when_done) {
+    pdl_wait();
     if (skip_when_done && sc->done) return;
     __shared__ double sv[8];
     __shared__ double sv2[1024];
@@ -531,8 +532,8 @@ static void launch_dot_f(const LD &ld, int64_t n, double *tmp, double *out_dev, 
         // ticket zeroed at allocation and re-armed to 0 by the last block
         unsigned *ticket = reinterpret_cast<unsigned *>(tmp);
         const unsigned grid = (unsigned)std::min<int64_t>(nb1, 148 * kDotBlocksPerSM);
-        k_dot_fused<LD><<<grid, 256, 0, st>>>(ld, n, cut, p0, ticket, epi, sc, out_dev,
-                                              skip ? 1 : 0);
+        launch_pdl(k_dot_fused<LD>, grid, 256, 0, st, ld, n, cut, p0, ticket, epi, sc, out_dev,
+                   skip ? 1 : 0);
         (*launches)++;
         return;
     }
@@ -635,6 +636,7 @@ __global__ void k_compact_nbr(SysView S, unsigned short *__restrict__ meta,
 // order as nbr_sum, so the result is bit-identical.
 __global__ void __launch_bounds__(256)
 k_matvec_c(SysView S, const double *__restrict__ x, double *__restrict__ y, const DevScalars *sc) {
+    pdl_wait();
     if (sc->done) return;
     for (int64_t r = gtid(); r < S.n; r += gstride()) {
         const unsigned m = S.meta[r];
@@ -964,6 +966,7 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
              const double *__restrict__ s, const double *__restrict__ q, DevScalars *sc,
              double *__restrict__ rL, const int *__restrict__ posL, int64_t max_iters,
              double *history) {
+    pdl_wait();
     if (sc->done) return;
     __shared__ double wm[8];
     __shared__ bool last;
@@ -1038,6 +1041,7 @@ __global__ void k_inv_diag(int64_t n, const double *__restrict__ diag, double sc
 // s = z + beta s (pressure.py:329)
 __global__ void k_pcg_dir(int64_t n, double *__restrict__ s, const double *__restrict__ z,
                           const DevScalars *sc) {
+    pdl_wait();
     if (sc->done) return;
     double beta = sc->beta;
     for (int64_t i = gtid(); i < n; i += gstride()) s[i] = z[i] + beta * s[i];
@@ -1239,24 +1243,23 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                                  st, launches);
                 } else {
                     if (S.meta)
-                        k_matvec_c<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, sc);
+                        launch_pdl(k_matvec_c, nblocks(n), kThreads, 0, st, S, B.s, B.q, sc);
                     else
                         k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
                                                                   nullptr, sc, 1);
                     launch_dot(B.s, B.q, n, B.dot_tmp, nullptr, EPI_CURV, sc, st, launches);
                     (*launches)++;
                 }
-                k_pcg_update<<<nblocks(n), kThreads, 0, st>>>(n, B.x, B.r, B.s, B.q, sc,
-                                                              lane ? LV.lane->rL : nullptr,
-                                                              lane ? LV.lane->posL : nullptr,
-                                                              cfg.max_iters, cfg.history);
+                launch_pdl(k_pcg_update, nblocks(n), kThreads, 0, st, n, B.x, B.r, B.s, B.q, sc,
+                           lane ? LV.lane->rL : nullptr, lane ? LV.lane->posL : nullptr,
+                           (int64_t)cfg.max_iters, cfg.history);
                 apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
                 if (lane)
                     launch_dot_f(LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, n, B.dot_tmp,
                                  nullptr, EPI_SIGMA_NEW, sc, st, launches);
                 else
                     launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA_NEW, sc, st, launches);
-                k_pcg_dir<<<nblocks(n), kThreads, 0, st>>>(n, B.s, B.z, sc);
+                launch_pdl(k_pcg_dir, nblocks(n), kThreads, 0, st, n, B.s, B.z, sc);
                 *launches += 2;  // update (with the convergence test) + dir
             } else {  // pressure.py:209-213
                 if (cfg.solver == FLIP_SOLVER_JACOBI) {

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(CT *CT + 32) k_mic_cl(LaneArgs A) {
     // yring[nsteps][TZ], zring[nsteps][TY], then the operand chunks
     extern __shared__ __align__(128) double ring[];
     const int t = threadIdx.x;
+    pdl_wait();
     if (A.sc && A.sc->done) return;  // same value in every CTA of the launch
     const WaveGeom G = A.geom;
     const int nsteps = G.nsteps;
@@ -450,13 +451,15 @@ static cudaError_t launch_cl_k(const LaneArgs &A, cudaStream_t st) {
     cfg.blockDim = dim3(CT * CT + 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CY * CZ;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl_wait() in the kernel
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_cl<REV, CY, CZ, KC, NB, L2AHEAD>, A);
     return e != cudaSuccess ? e : cudaPeekAtLastError();
 }

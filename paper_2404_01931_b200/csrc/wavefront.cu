@@ -876,6 +876,7 @@ __global__ void k_wave_prep(double *halo, int64_t nh, int *ticket, const DevScal
 __global__ void k_wave_prep_cl(double *halo_y, double *halo_z, int TB, int TC, int nsteps, int ty,
                                int tz, int cy, int cz, int rev, int *ticket,
                                const DevScalars *sc) {
+    pdl_wait();
     if (sc && sc->done) return;
     if (gtid() == 0) *ticket = 0;
     const double m = __longlong_as_double((long long)WAVE_PENDING);
@@ -1043,9 +1044,9 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
     if (try_cluster && !full_prep) {
         const int64_t nsel = (int64_t)(A.geom.TB / cy) * A.geom.TC * A.geom.nsteps * TZ +
                              (int64_t)A.geom.TB * (A.geom.TC / cz) * A.geom.nsteps * TY;
-        k_wave_prep_cl<<<nblocks(nsel), kThreads, 0, st>>>(
-            A.halo_y, A.halo_y + tiles * A.geom.nsteps * TZ, A.geom.TB, A.geom.TC, A.geom.nsteps,
-            TY, TZ, cy, cz, REV ? 1 : 0, A.ticket, A.sc);
+        launch_pdl(k_wave_prep_cl, nblocks(nsel), kThreads, 0, st, A.halo_y,
+                   A.halo_y + tiles * A.geom.nsteps * TZ, A.geom.TB, A.geom.TC, A.geom.nsteps, TY,
+                   TZ, cy, cz, REV ? 1 : 0, A.ticket, A.sc);
     } else {
         k_wave_prep<<<nblocks(nh), kThreads, 0, st>>>(A.halo_y, nh, A.ticket, A.sc);
     }
