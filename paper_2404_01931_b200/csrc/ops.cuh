@@ -175,6 +175,18 @@ inline void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_
     cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// One resident wave of k (grid-stride kernels), from the occupancy calculator.
+template <typename K>
+inline unsigned wave_blocks(K k, int64_t n, int threads = kThreads) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    int64_t b = (n + threads - 1) / threads, cap = 148 * (int64_t)per_sm;
+    return (unsigned)(b < 1 ? 1 : b > cap ? cap : b);
+}
+
 inline unsigned nblocks(int64_t n, int threads = kThreads, int64_t cap = 148 * 32) {
     int64_t b = (n + threads - 1) / threads;
     if (b < 1) b = 1;

@@ -1243,14 +1243,14 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                                  st, launches);
                 } else {
                     if (S.meta)
-                        launch_pdl(k_matvec_c, nblocks(n), kThreads, 0, st, S, B.s, B.q, sc);
+                        launch_pdl(k_matvec_c, wave_blocks(k_matvec_c, n), kThreads, 0, st, S, B.s, B.q, sc);
                     else
                         k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
                                                                   nullptr, sc, 1);
                     launch_dot(B.s, B.q, n, B.dot_tmp, nullptr, EPI_CURV, sc, st, launches);
                     (*launches)++;
                 }
-                launch_pdl(k_pcg_update, nblocks(n), kThreads, 0, st, n, B.x, B.r, B.s, B.q, sc,
+                launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n, B.x, B.r, B.s, B.q, sc,
                            lane ? LV.lane->rL : nullptr, lane ? LV.lane->posL : nullptr,
                            (int64_t)cfg.max_iters, cfg.history);
                 apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
@@ -1259,7 +1259,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                                  nullptr, EPI_SIGMA_NEW, sc, st, launches);
                 else
                     launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA_NEW, sc, st, launches);
-                launch_pdl(k_pcg_dir, nblocks(n), kThreads, 0, st, n, B.s, B.z, sc);
+                launch_pdl(k_pcg_dir, wave_blocks(k_pcg_dir, n), kThreads, 0, st, n, B.s, B.z, sc);
                 *launches += 2;  // update (with the convergence test) + dir
             } else {  // pressure.py:209-213
                 if (cfg.solver == FLIP_SOLVER_JACOBI) {
