@@ -71,6 +71,10 @@ extern "C" {
  * the reference (which has only MIC(0)) and are validated to tolerance */
 #define FLIP_PRECOND_MG 3
 
+/* ---- advection schemes (extension; the reference is forward Euler) ---- */
+#define FLIP_ADVECT_EULER 0
+#define FLIP_ADVECT_RK2 1
+
 typedef struct flip_ctx flip_ctx;
 
 /* SceneSpec (sim.py:50-72) as the step consumes it.  The *_h fields are the
@@ -93,7 +97,8 @@ typedef struct {
     int32_t density;
     uint64_t reseed_seed;  /* rng.derive_seed(rng_seed, step_count + 1) (sim.py:291) */
     int32_t solver_check_every; /* PCG/relaxation convergence poll period (perf knob; 0 = auto) */
-    int32_t reserved;
+    int32_t advection;     /* FLIP_ADVECT_EULER (the reference, particles.py:227-248) or
+                              FLIP_ADVECT_RK2 (extension: midpoint through the grid) */
 } flip_step_params;
 
 /* StepReport (sim.py:87-93) plus diagnostics. */
@@ -123,6 +128,8 @@ typedef struct {
 } flip_region;
 
 const char *flip_last_error(void);
+/* SingularSystemError.cell of the last FLIP_E_SINGULAR on this thread, else -1. */
+int64_t flip_last_error_cell(void);
 int flip_device_count(int *count);
 
 /* ctx lifecycle.  capacity is the initial particle-buffer size; <= 0 picks
@@ -201,6 +208,10 @@ typedef struct {
     int64_t capacity, n;
 } flip_dev_ptrs;
 int flip_get_dev_ptrs(flip_ctx *ctx, flip_dev_ptrs *out);
+/* Grow the particle buffers (keeping the live particles) so that at least n
+ * fit; device pointers from flip_get_dev_ptrs are invalidated if they move.
+ * Call before writing more than `capacity` rows into the device views. */
+int flip_reserve_particles(flip_ctx *ctx, int64_t n);
 /* The particle arrays were rewritten in place (device) with n particles, in
  * any order: the next FLIP_STAGE_BIN recomputes the keys. */
 int flip_set_particle_count(flip_ctx *ctx, int64_t n);

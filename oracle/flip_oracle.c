@@ -285,6 +285,50 @@ void orc_sample_velocity_many(const orc_dims *d, const double *u, const double *
     }
 }
 
+/* Extension, opt-in (SceneSpec.advection = "rk2"): explicit-midpoint RK2
+ * through the grid velocity field the previous step left (the north star
+ * names "RK2 particle advection"; the reference itself is forward Euler on
+ * the particle velocities, F/particles.py:227-248, and SPEC.md:211 lists
+ * RK2 as a non-goal, so this restatement is the only definition):
+ *   k1 = sample(grid, p)            (F/_kernels/_core.pyx:68-90 sampling)
+ *   m  = p + (k1 * (0.5 * dt))
+ *   k2 = sample(grid, m)
+ *   p' = p + (k2 * dt), then the reference's per-axis clamp
+ *        (<= lo -> lo + skin, >= hi -> hi - skin, F/particles.py:237-247).
+ * Particle velocities are not touched (as in the Euler advect). */
+static inline void sample3(const orc_dims *d, const double *u, const double *v, const double *w,
+                           double x, double y, double z, double out[3]) {
+    int64_t nx = d->nx, ny = d->ny, nz = d->nz;
+    double gx = (x - d->ox) / d->dtau;
+    double gy = (y - d->oy) / d->dtau;
+    double gz = (z - d->oz) / d->dtau;
+    out[0] = tri_one(u, nx + 1, ny, nz, gx, gy - 0.5, gz - 0.5);
+    out[1] = tri_one(v, nx, ny + 1, nz, gx - 0.5, gy, gz - 0.5);
+    out[2] = tri_one(w, nx, ny, nz + 1, gx - 0.5, gy - 0.5, gz);
+}
+
+void orc_advect_rk2(const orc_dims *d, const double *u, const double *v, const double *w,
+                    int64_t n, double *px, double *py, double *pz, double dt,
+                    const double lo[3], const double hi[3], double skin) {
+    const double h = 0.5 * dt;
+    #pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < n; t++) {
+        double p[3] = {px[t], py[t], pz[t]}, k1[3], k2[3], m[3];
+        sample3(d, u, v, w, p[0], p[1], p[2], k1);
+        for (int a = 0; a < 3; a++) m[a] = p[a] + (k1[a] * h);
+        sample3(d, u, v, w, m[0], m[1], m[2], k2);
+        for (int a = 0; a < 3; a++) {
+            double q = p[a] + (k2[a] * dt);
+            if (q <= lo[a]) q = lo[a] + skin;
+            else if (q >= hi[a]) q = hi[a] - skin;
+            p[a] = q;
+        }
+        px[t] = p[0];
+        py[t] = p[1];
+        pz[t] = p[2];
+    }
+}
+
 /* ---------------------------------------------------------------- P2G -- */
 static inline double hat(double r) {  /* F/_kernels/_core.pyx:17-19 */
     r = fabs(r);

@@ -61,6 +61,9 @@ void orc_bin_particles(const orc_dims *d, int64_t n, double *arrs[6], double *sc
 void orc_classify_cells(int64_t ncells, const int64_t *count, uint8_t *label);
 
 /* _core.pyx:68-90 */
+void orc_advect_rk2(const orc_dims *d, const double *u, const double *v, const double *w,
+                    int64_t n, double *px, double *py, double *pz, double dt,
+                    const double lo[3], const double hi[3], double skin);
 void orc_sample_velocity_many(const orc_dims *d, const double *u, const double *v, const double *w,
                               int64_t n, const double *px, const double *py, const double *pz,
                               double *vx, double *vy, double *vz);

@@ -10,7 +10,8 @@ restatement of each reference function.  Scene construction restates
 ``sim.py:96-223`` (scene_regions, _fit_box, make_scene).  Parity of this
 oracle with the real reference is pinned by ``tests/golden/`` fixtures
 (generated from the reference by ``tests/golden/make_golden.py``) and, in the
-build container, by ``tests/test_oracle_vs_reference.py`` directly.
+build container, by ``tests/test_oracle_pins.py::test_oracle_equals_live_reference_40cubed``
+(the live reference, skipped where /root/reference is absent).
 """
 
 from __future__ import annotations
@@ -78,6 +79,8 @@ def lib():
             "orc_compute_dt": (C.c_double, [C.c_int64, _d, _d, _d, C.c_double, C.c_double,
                                             C.c_double]),
             "orc_interior_box": (C.c_int, [P(Dims), _u8, _d, _d]),
+            "orc_advect_rk2": (None, [P(Dims), _d, _d, _d, C.c_int64, _d, _d, _d, C.c_double,
+                                      _d, _d, C.c_double]),
             "orc_advect": (None, [C.c_int64, _d, _d, _d, _d, _d, _d, C.c_double, _d, _d,
                                   C.c_double]),
             "orc_cell_index_many": (None, [P(Dims), C.c_int64, _d, _d, _d, _i64]),
@@ -161,6 +164,7 @@ class Spec:
     steps: int = 50
     precond: str = "mic0"   # not in SceneSpec; the reference hard-wires mic0 (pressure.py:274)
     obstacles: tuple = ()   # extension: SOLID cell boxes after the shell
+    advection: str = "euler"  # extension: "rk2" = orc_advect_rk2 (the reference is Euler only)
 
     def resolved_max_iters(self) -> int:
         if self.max_iters is not None:
@@ -427,9 +431,13 @@ def interior_box(st: OState):
     return lo, hi
 
 
-def advect(st: OState, dt: float, skin: float) -> None:
+def advect(st: OState, dt: float, skin: float, scheme: str = "euler") -> None:
     lo, hi = interior_box(st)
     P = st.parts
+    if scheme == "rk2":
+        lib().orc_advect_rk2(C.byref(st.dims.c()), _p(st.u), _p(st.v), _p(st.w), st.n,
+                             _p(P[0]), _p(P[1]), _p(P[2]), dt, _p(lo), _p(hi), skin)
+        return
     lib().orc_advect(st.n, _p(P[0]), _p(P[1]), _p(P[2]), _p(P[3]), _p(P[4]), _p(P[5]),
                      dt, _p(lo), _p(hi), skin)
 
@@ -624,7 +632,7 @@ def step(st: OState, spec: Spec, hook=None) -> dict:
     mark("dt_compute", t0, dt=dt)
 
     t0 = clock()
-    advect(st, dt, spec.skin_fraction * st.dims.dtau)
+    advect(st, dt, spec.skin_fraction * st.dims.dtau, spec.advection)
     mark("advect", t0)
 
     t0 = clock()

@@ -47,7 +47,7 @@ class StepParams(C.Structure):
         ("density", C.c_int32),
         ("reseed_seed", C.c_uint64),
         ("solver_check_every", C.c_int32),
-        ("reserved", C.c_int32),
+        ("advection", C.c_int32),
     ]
 
 
@@ -140,6 +140,8 @@ _SIGNATURES = {
     "flip_energy_sums": (C.c_int, [_vp, C.c_double, _d, _d]),
     "flip_get_dev_ptrs": (C.c_int, [_vp, C.POINTER(DevPtrs)]),
     "flip_set_particle_count": (C.c_int, [_vp, C.c_int64]),
+    "flip_reserve_particles": (C.c_int, [_vp, C.c_int64]),
+    "flip_last_error_cell": (C.c_int64, []),
     "flip_set_slab": (C.c_int, [_vp, C.c_int64, C.c_int64]),
     "flip_particle_cells": (C.c_int, [_vp, _vp]),
     "flip_k_sample_velocity_many": (C.c_int, [_d, _d, _d, C.c_int64, C.c_int64, C.c_int64,
@@ -203,6 +205,9 @@ def check(rc: int, what: str = "") -> None:
     if rc == FLIP_E_CAPACITY:
         raise MemoryError(msg)
     if rc == FLIP_E_SINGULAR:
+        cell = int(LIB.flip_last_error_cell())
+        if cell >= 0:
+            raise errors.SingularSystemError(cell)
         raise errors.SolverError(msg)
     if rc == FLIP_E_BREAKDOWN:
         raise errors.SolverBreakdownError(msg)

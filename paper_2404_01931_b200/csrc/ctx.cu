@@ -2,7 +2,10 @@
 // transfer, the step orchestrator and the particle-side plugin kernels.
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "ops.cuh"
 #include "wavefront.cuh"
@@ -10,7 +13,43 @@
 namespace flip {
 
 static thread_local std::string g_err;
-void set_error(const std::string &msg) { g_err = msg; }
+static thread_local int64_t g_err_cell = -1;
+void set_error(const std::string &msg) {
+    g_err = msg;
+    g_err_cell = -1;
+}
+void set_error_cell(int64_t cell) { g_err_cell = cell; }
+
+int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+            n = 148;
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
+int occupancy_per_sm(const void *fn, int threads) {
+    // (kernel, device, threads) -> resident CTAs per SM; a handful of entries
+    struct Ent { const void *fn; int dev, threads, per_sm; };
+    static std::vector<Ent> cache;
+    static std::mutex mu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Ent &e : cache)
+        if (e.fn == fn && e.dev == dev && e.threads == threads) return e.per_sm;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+    if (per_sm < 1) per_sm = 1;
+    cache.push_back({fn, dev, threads, per_sm});
+    return per_sm;
+}
 
 Dims make_dims(int64_t nx, int64_t ny, int64_t nz, double dtau, const double origin[3]) {
     Dims d{};
@@ -71,6 +110,7 @@ using namespace flip;
 struct flip_ctx : public Ctx {};
 
 extern "C" const char *flip_last_error(void) { return g_err.c_str(); }
+extern "C" int64_t flip_last_error_cell(void) { return g_err_cell; }
 
 extern "C" int flip_device_count(int *count) {
     FLIP_CUDA_OK(cudaGetDeviceCount(count));
@@ -403,6 +443,15 @@ extern "C" int flip_get_dev_ptrs(flip_ctx *c, flip_dev_ptrs *o) {
     return 0;
 }
 
+extern "C" int flip_reserve_particles(flip_ctx *c, int64_t n) {
+    if (n < 0) {
+        set_error("negative particle count");
+        return FLIP_E_ARG;
+    }
+    cudaSetDevice(c->device);
+    return reserve_particles(*c, n);
+}
+
 extern "C" int flip_set_particle_count(flip_ctx *c, int64_t n) {
     if (n < 0 || n > c->cap) {
         set_error("particle count exceeds capacity");
@@ -603,7 +652,19 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
     int64_t launches0 = c->launches;
     bool keys_from_advect = false, force_fused = false, reseed_ran = false;
     int status = 0;
+    // NVTX: one range per stage (StageTimings keys, sim.py:24-46), visible
+    // to nsys / ncu --nvtx; a no-op without an attached tool
+    static const char *kStageNames[FLIP_NSTAGES] = {
+        "flip/dt_compute", "flip/advect", "flip/bin", "flip/classify", "flip/p2g",
+        "flip/force", "flip/project", "flip/apply_gradient", "flip/g2p", "flip/reseed"};
+    struct NvtxRange {
+        bool on = false;
+        void push(const char *n) { nvtxRangePushA(n); on = true; }
+        ~NvtxRange() { if (on) nvtxRangePop(); }
+    };
     for (int s = first; s <= last && !status; s++) {
+        NvtxRange nv;
+        nv.push(kStageNames[s]);
         cudaEventRecord(c->ev[s], c->st);
         switch (s) {
             case FLIP_STAGE_DT:
@@ -674,6 +735,7 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
     rep->gpu_launches = c->launches - launches0;
     if (status) {
         set_error(status == FLIP_E_SINGULAR ? "singular pressure system" : "conjugate-gradient breakdown");
+        if (status == FLIP_E_SINGULAR) set_error_cell(rep->err_cell);
         return status;
     }
     return 0;

@@ -127,7 +127,9 @@ __global__ void k_mg_jacobi(MgLevel L, const double *__restrict__ xin, double *_
                             double w, const DevScalars *sc) {
     if (sc && sc->done) return;
     for (int64_t q = gtid(); q < L.nc; q += gstride()) {
-        if (L.type[q] != MG_ROW) {
+        // an isolated coarse ROW cell (every neighbour SOLID, diag 0) has
+        // no equation to relax: leave it at 0 instead of dividing by 0
+        if (L.type[q] != MG_ROW || L.diag[q] == 0) {
             xout[q] = 0.0;
             continue;
         }
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(1024) k_mg_coarse(MgLevel L, int sweeps, doubl
     double *cur = xa, *nxt = xb;
     for (int it = 0; it < sweeps; it++) {
         for (int q = threadIdx.x; q < nc; q += blockDim.x) {
-            if (L.type[q] != MG_ROW) {
+            if (L.type[q] != MG_ROW || L.diag[q] == 0) {  // isolated: see k_mg_jacobi
                 nxt[q] = 0.0;
                 continue;
             }

@@ -175,20 +175,24 @@ inline void launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_
     cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// Streaming-multiprocessor count of the current device (queried once per
+// device; 148 on B200, fewer on MIG slices or other parts).
+int num_sms();
+// Resident CTAs per SM of kernel fn at `threads` threads (cached per kernel
+// and device).
+int occupancy_per_sm(const void *fn, int threads);
+
 // One resident wave of k (grid-stride kernels), from the occupancy calculator.
 template <typename K>
 inline unsigned wave_blocks(K k, int64_t n, int threads = kThreads) {
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, 0);
-        if (per_sm < 1) per_sm = 1;
-    }
-    int64_t b = (n + threads - 1) / threads, cap = 148 * (int64_t)per_sm;
+    const int per_sm = occupancy_per_sm((const void *)k, threads);
+    int64_t b = (n + threads - 1) / threads, cap = (int64_t)num_sms() * per_sm;
     return (unsigned)(b < 1 ? 1 : b > cap ? cap : b);
 }
 
-inline unsigned nblocks(int64_t n, int threads = kThreads, int64_t cap = 148 * 32) {
-    int64_t b = (n + threads - 1) / threads;
+// Grid-stride grid: enough CTAs for n, at most `per_sm` per SM.
+inline unsigned nblocks(int64_t n, int threads = kThreads, int64_t per_sm = 32) {
+    int64_t b = (n + threads - 1) / threads, cap = (int64_t)num_sms() * per_sm;
     if (b < 1) b = 1;
     if (b > cap) b = cap;
     return (unsigned)b;
@@ -198,6 +202,8 @@ inline unsigned nblocks(int64_t n, int threads = kThreads, int64_t cap = 148 * 3
 Dims make_dims(int64_t nx, int64_t ny, int64_t nz, double dtau, const double origin[3]);
 
 void set_error(const std::string &msg);
+// SingularSystemError.cell of the last FLIP_E_SINGULAR (after set_error).
+void set_error_cell(int64_t cell);
 
 #define FLIP_CUDA_OK(expr)                                                                 \
     do {                                                                                   \

@@ -101,6 +101,36 @@ __global__ void k_advect_key(ParticlePtrs P, int64_t n, const DevScalars *__rest
     }
 }
 
+// Extension (SceneSpec.advection = "rk2"): explicit-midpoint RK2 through
+// the grid velocity field left by the previous step, then the reference's
+// per-axis clamp; restated in oracle/flip_oracle.c (orc_advect_rk2).  The
+// reference advects by forward Euler only (particles.py:227-248).
+__global__ void k_advect_rk2_key(ParticlePtrs P, int64_t n, const DevScalars *__restrict__ sc,
+                                 double skin, Dims d, const double *__restrict__ u,
+                                 const double *__restrict__ v, const double *__restrict__ w,
+                                 int *__restrict__ keys, int *__restrict__ count) {
+    const double dt = sc->dt, h = 0.5 * dt;
+    double lo[3] = {sc->lo[0], sc->lo[1], sc->lo[2]}, hi[3] = {sc->hi[0], sc->hi[1], sc->hi[2]};
+    for (int64_t t = gtid(); t < n; t += gstride()) {
+        double p[3] = {P.a[0][t], P.a[1][t], P.a[2][t]}, k1[3], k2[3], m[3];
+        sample_vel(d, u, v, w, p[0], p[1], p[2], k1[0], k1[1], k1[2]);
+#pragma unroll
+        for (int a = 0; a < 3; a++) m[a] = p[a] + (k1[a] * h);
+        sample_vel(d, u, v, w, m[0], m[1], m[2], k2[0], k2[1], k2[2]);
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            double q = p[a] + (k2[a] * dt);
+            if (q <= lo[a]) q = lo[a] + skin;
+            else if (q >= hi[a]) q = hi[a] - skin;
+            P.a[a][t] = q;
+            p[a] = q;
+        }
+        int cell = cell_of(d, p[0], p[1], p[2]);
+        keys[t] = cell;
+        atomicAdd(&count[cell], 1);
+    }
+}
+
 void stage_advect(Ctx &c, const flip_step_params &prm) {
     // interior_box (grid.py:121-132) depends only on the SOLID cells, which no
     // stage changes: recomputed after a label setter invalidated it
@@ -112,7 +142,11 @@ void stage_advect(Ctx &c, const flip_step_params &prm) {
         c.box_valid = 1;
     }
     cudaMemsetAsync(c.count, 0, sizeof(int) * c.ncells, c.st);
-    if (c.n > 0) {
+    if (c.n > 0 && prm.advection == FLIP_ADVECT_RK2) {
+        k_advect_rk2_key<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.sc, prm.skin_h, c.d, c.u,
+                                                              c.v, c.w, c.keys0, c.count);
+        c.launches++;
+    } else if (c.n > 0) {
         k_advect_key<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.sc, prm.skin_h, c.d, c.keys0,
                                                           c.count);
         c.launches++;

@@ -531,7 +531,7 @@ static void launch_dot_f(const LD &ld, int64_t n, double *tmp, double *out_dev, 
     if (nb1 <= 1024) {
         // ticket zeroed at allocation and re-armed to 0 by the last block
         unsigned *ticket = reinterpret_cast<unsigned *>(tmp);
-        const unsigned grid = (unsigned)std::min<int64_t>(nb1, 148 * kDotBlocksPerSM);
+        const unsigned grid = (unsigned)std::min<int64_t>(nb1, (int64_t)num_sms() * kDotBlocksPerSM);
         launch_pdl(k_dot_fused<LD>, grid, 256, 0, st, ld, n, cut, p0, ticket, epi, sc, out_dev,
                    skip ? 1 : 0);
         (*launches)++;
@@ -1108,6 +1108,13 @@ struct SweepLevels {
     Ctx *mg = nullptr;     // multigrid preconditioner state (FLIP_PRECOND_MG)
 };
 
+// First sweep-launch failure of the current solve (configuration errors
+// such as a shared-memory request are not sticky CUDA errors, and
+// cudaGetLastError in the launchers clears them).  Per host thread, like
+// the error message, so contexts driven from different threads (one per
+// GPU) never see each other's failures.
+static thread_local cudaError_t g_sweep_launch_err = cudaSuccess;
+
 template <int MODE>
 static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src, double *dst,
                      const double *precon, DevScalars *sc, cudaStream_t st, int64_t *launches) {
@@ -1128,7 +1135,10 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
             pb->launches++;
             pb->bytes += 24.0 * (double)A.n;  // src + precon read, dst written: 3 x 8 B per row
         }
-        if (e != cudaSuccess) set_error(std::string("wavefront launch: ") + cudaGetErrorString(e));
+        if (e != cudaSuccess) {
+            set_error(std::string("wavefront launch: ") + cudaGetErrorString(e));
+            if (g_sweep_launch_err == cudaSuccess) g_sweep_launch_err = e;  // fails the solve
+        }
         *launches += 2;
         return;
     }
@@ -1138,9 +1148,6 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
 }
 
 // z = M^-1 r for the selected preconditioner (pressure.py:284-300).
-// First sweep-launch failure of the current solve (configuration errors
-// such as a shared-memory request are not sticky CUDA errors).
-static cudaError_t g_sweep_launch_err = cudaSuccess;
 
 // fused: the lane path's r -> L and L -> z conversions are done by the
 // caller's k_pcg_update and z.r dot (r already in Lb.rL, z left in Lb.zL).
@@ -1169,7 +1176,7 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             cudaError_t e = launch_mic_lane(rev != 0, A, st);
             if (e != cudaSuccess) {
                 set_error(std::string("lane sweep launch: ") + cudaGetErrorString(e));
-                g_sweep_launch_err = e;  // fails the solve (stage_project)
+                if (g_sweep_launch_err == cudaSuccess) g_sweep_launch_err = e;  // fails the solve
             }
             if (probed) {
                 cudaEventRecord(pb->ev[2 * pb->used + 1], st);
@@ -1760,5 +1767,11 @@ extern "C" int flip_solve_system(int32_t solver, int32_t precond, int64_t n, con
     *err_cell = o.err_cell;
     *err_iteration = o.err_it;
     *err_value = o.err_value;
+    if (o.status == FLIP_E_SINGULAR) {
+        set_error("singular pressure system");
+        set_error_cell(o.err_cell);
+    } else if (o.status == FLIP_E_BREAKDOWN) {
+        set_error("conjugate-gradient breakdown");
+    }
     return o.status;
 }

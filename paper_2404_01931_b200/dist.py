@@ -259,9 +259,10 @@ def _write_particles(dev, rows) -> None:
     import torch
     p = _ptrs(dev)
     m = int(rows.shape[0])
-    if m > p.capacity:
-        raise RuntimeError(f"slab holds {m} particles, capacity {p.capacity}")
     torch.cuda.synchronize()
+    if m > p.capacity:  # grow first (keeps nothing we need: rows is a copy)
+        check(LIB.flip_reserve_particles(dev.ctx, m), "flip_reserve_particles")
+        p = _ptrs(dev)
     for a in range(6):
         ptr = p.pos[a] if a < 3 else p.vel[a - 3]
         if m:

@@ -25,6 +25,7 @@ from .particles import ParticleSet, SeedRegion, covered_cells
 SCENE_NAMES = ("dam-break", "double-dam-break", "water-drop", "double-dam-break-obstacle")
 SOLVERS = ("jacobi", "gs", "rbgs", "pcg")
 PRECONDITIONERS = ("mic0", "jacobi", "none", "mg")   # "mg": extension, tolerance-validated
+ADVECTION = ("euler", "rk2")   # "rk2": extension, restated in oracle/flip_oracle.c
 
 
 @dataclass
@@ -81,6 +82,9 @@ class SceneSpec:
     # scene extension: extra SOLID cell boxes
     # (i0, i1, j0, j1, k0, k1), inclusive, applied after the wall shell
     obstacles: tuple = ()
+    # extension: "rk2" advects by explicit midpoint through the grid velocity
+    # field (north star); the reference is forward Euler (particles.py:227-248)
+    advection: str = "euler"
 
     def resolved_max_iters(self) -> int:
         if self.max_iters is not None:
@@ -205,6 +209,8 @@ def _params(cfg: SceneSpec, dtau: float, reseed_seed: int = 0) -> _lib.StepParam
         raise ConfigError(f"unknown solver {cfg.solver!r}; valid: {SOLVERS}")
     if cfg.precond not in PRECONDITIONERS:
         raise ValueError(f"unknown preconditioner {cfg.precond!r}")
+    if cfg.advection not in ADVECTION:
+        raise ConfigError(f"unknown advection scheme {cfg.advection!r}; valid: {ADVECTION}")
     if not 0.0 <= cfg.flip_fraction <= 1.0:           # BlendParams (transfer.py:16-24)
         raise ValueError("flip_fraction must lie in [0, 1]")
     assert cfg.alpha > 0 and cfg.dt_max > 0             # particles.py:217
@@ -226,6 +232,7 @@ def _params(cfg: SceneSpec, dtau: float, reseed_seed: int = 0) -> _lib.StepParam
     p.density = int(cfg.density)
     p.reseed_seed = int(reseed_seed) & rng.MASK64
     p.solver_check_every = 0
+    p.advection = ADVECTION.index(cfg.advection)
     return p
 
 

@@ -14,6 +14,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: longer parity cases")
 
 
+def pytest_collection_modifyitems(config, items):
+    """`slow` cases (minutes, tens of GB of host RAM) run only when the
+    marker expression asks for them (-m slow / -m "gpu and slow")."""
+    if "slow" in (config.getoption("-m") or ""):
+        return
+    skip = pytest.mark.skip(reason="slow: select with -m slow")
+    for item in items:
+        if "slow" in item.keywords:
+            item.add_marker(skip)
+
+
 @pytest.fixture(scope="session")
 def oracle():
     import oracle as O

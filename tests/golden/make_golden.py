@@ -106,7 +106,8 @@ def main():
     # ---- kernel-level goldens (inputs = the reference tests' seeded inputs)
     from flipsim._kernels import _core as K
     from flipsim.binning import bin_particles, cell_index_many
-    from flipsim.grid import GridDims, MacGrid, enforce_solid_boundaries, set_solid_shell, FLUID
+    from flipsim.grid import (GridDims, MacGrid, divergence_field, enforce_solid_boundaries,
+                              set_solid_shell, FLUID)
     from flipsim.particles import ParticleSet
     from flipsim.pressure import assemble, SOLVERS, solve_pcg
     import functools
@@ -181,6 +182,15 @@ def main():
                                        "residual": float(res.residual).hex(),
                                        "converged": bool(res.converged)}
         kout[key] = rec
+        # divergence_field (grid.py:147-156) of the same random velocity field
+        kout[f"divergence_{n}_seed{seed}"] = digest(divergence_field(g))
+    # divergence_field of a scene state after two steps (non-trivial u/v/w)
+    spec = RS.SceneSpec(name="dam-break", res=20, solver="pcg")
+    st = RS.make_scene(spec, rng_seed=6)
+    for _ in range(2):
+        RS.step(st, spec)
+    kout["divergence_dam_break_20_seed6_step2"] = {"grid": digest(divergence_field(st.grid)),
+                                                   "u": digest(st.grid.u)}
     json.dump({"generator": "tests/golden/make_golden.py", "kernels": kout},
               open(os.path.join(HERE, "reference_kernels.json"), "w"), indent=1)
     print("wrote goldens")

@@ -24,6 +24,9 @@ STEP_CASES = [
     dict(name="double-dam-break", res=18, solver="pcg", precond="none", flip_fraction=0.0),
     dict(name="double-dam-break-obstacle", res=24, solver="pcg"),
     dict(name="water-drop", res=20, solver="rbgs", obstacles=((3, 6, 1, 3, 3, 16), (12, 14, 2, 8, 5, 9))),
+    # extension: RK2 (explicit midpoint through the grid) vs orc_advect_rk2
+    dict(name="dam-break", res=16, solver="pcg", advection="rk2"),
+    dict(name="double-dam-break-obstacle", res=20, solver="jacobi", advection="rk2"),
 ]
 
 
@@ -181,17 +184,95 @@ def test_multicluster_sweep_bit_exact(pkg, case):
         assert rep.solver_residual == ref["solver_residual"]
 
 
-def test_full_size_step_bit_exact(pkg):
+def test_full_size_steps_bit_exact(pkg):
     """BASELINE's full size: the 256^3 dam-break (24.7M particles) make_scene
-    and one step, every byte equal to the oracle's."""
+    and three steps, every byte equal to the oracle's after each step.  Step 1
+    starts from zero velocities (advect and the P2G values are trivial);
+    steps 2 and 3 exercise advect, binning of moved particles, P2G, the FLIP
+    blend and reseed on non-degenerate data at the BASELINE size."""
     dspec, ospec = spec_pair(name="dam-break", res=256, solver="pcg")
     st = pkg.make_scene(dspec, rng_seed=0)
     os_ = O.make_scene(ospec, rng_seed=0)
     assert st.particles.count == os_.parts[0].size > 24_000_000
+    for k in range(3):
+        rep = pkg.step(st, dspec)
+        ref = O.step(os_, ospec)
+        bad = diff_report(device_arrays(st), oracle_arrays(os_))
+        assert not bad, f"256^3 step {k + 1}: {bad}"
+        assert rep.dt == ref["dt"]
+        assert rep.particle_count == ref["particle_count"]
+        assert rep.solver_iterations == ref["solver_iterations"]
+        assert rep.solver_residual == ref["solver_residual"]
+        if k:
+            assert np.abs(st.particles.vel_y).max() > 0      # non-degenerate
+
+
+def test_full_size_step_from_oracle_state(pkg):
+    """One device step from the ORACLE's 256^3 state after step 2 (uploaded),
+    compared with the oracle's step 3: the device step is checked on the
+    reference's own non-degenerate input, independently of its own history."""
+    dspec, ospec = spec_pair(name="dam-break", res=256, solver="pcg")
+    os_ = O.make_scene(ospec, rng_seed=0)
+    for _ in range(2):
+        O.step(os_, ospec)
+    st = pkg.make_scene(dspec, rng_seed=0)
+    for _ in range(2):                       # step_count / time / reseed stream
+        st.step_count += 1
+    st.time = os_.time
+    upload(st, os_)
     rep = pkg.step(st, dspec)
     ref = O.step(os_, ospec)
     bad = diff_report(device_arrays(st), oracle_arrays(os_))
-    assert not bad, f"256^3 step: {bad}"
+    assert not bad, f"256^3 step 3 from the oracle state: {bad}"
+    assert rep.solver_iterations == ref["solver_iterations"]
+    assert rep.solver_residual == ref["solver_residual"]
+
+
+def test_divergence_field_bit_exact(pkg):
+    """divergence_field (grid.py:147-156) on the device == the oracle's
+    orc_divergence_field, byte for byte, on scene states after each step."""
+    dspec, ospec = spec_pair(name="double-dam-break-obstacle", res=24, solver="pcg")
+    st = pkg.make_scene(dspec, rng_seed=2)
+    os_ = O.make_scene(ospec, rng_seed=2)
+    for k in range(3):
+        pkg.step(st, dspec)
+        O.step(os_, ospec)
+        want = O.divergence_field(os_.dims, os_.u, os_.v, os_.w)
+        got = pkg.divergence_field(st)
+        assert got.tobytes() == want.tobytes(), f"step {k}"
+
+
+@pytest.mark.parametrize("n,seed", [(8, 7), (8, 14), (12, 300)])
+def test_divergence_field_reference_golden(pkg, n, seed):
+    """The device divergence of the reference tests' random velocity fields
+    against the digests produced by the real reference (make_golden.py)."""
+    from golden_util import digest, load
+    from test_oracle_pins import random_mask_velocities
+    dims, u, v, w, label = random_mask_velocities(n, seed)
+    dspec, _ = spec_pair(name="dam-break", res=n)
+    st = pkg.make_scene(dspec, rng_seed=0)
+    st.device.set_grid(u=u, v=v, w=w, label=label)
+    want = load("reference_kernels.json")["kernels"][f"divergence_{n}_seed{seed}"]
+    assert digest(pkg.divergence_field(st)) == want
+
+
+@pytest.mark.slow
+def test_config4_512_obstacle_bit_exact(pkg):
+    """BASELINE config 4's scene at full size: double-dam-break + obstacle at
+    512^3 (399M particles), make_scene and one step, every byte equal to the
+    oracle's (all host threads; several minutes).  Selected with -m slow."""
+    import os
+    O.set_threads(os.cpu_count() or 1)
+    dspec, ospec = spec_pair(name="double-dam-break-obstacle", res=512, solver="pcg")
+    st = pkg.make_scene(dspec, rng_seed=0, capacity=int(1.5 * 8 * 0.21 * 512 ** 3) + 4096)
+    os_ = O.make_scene(ospec, rng_seed=0)
+    assert st.particles.count == os_.n == 398_991_360
+    bad = diff_report(device_arrays(st), oracle_arrays(os_))
+    assert not bad, f"make_scene: {bad}"
+    rep = pkg.step(st, dspec)
+    ref = O.step(os_, ospec)
+    bad = diff_report(device_arrays(st), oracle_arrays(os_))
+    assert not bad, f"512^3 step: {bad}"
     assert rep.solver_iterations == ref["solver_iterations"]
     assert rep.solver_residual == ref["solver_residual"]
 

@@ -90,3 +90,7 @@ def test_params_match_reference_host_arithmetic(pkg):
         sim._params(pkg.SceneSpec(flip_fraction=1.5), dtau)
     with pytest.raises(pkg.ConfigError):
         sim._params(pkg.SceneSpec(solver="multigrid"), dtau)
+    assert sim._params(spec, dtau).advection == 0                    # forward Euler default
+    assert sim._params(pkg.SceneSpec(advection="rk2"), dtau).advection == 1
+    with pytest.raises(pkg.ConfigError):
+        sim._params(pkg.SceneSpec(advection="rk4"), dtau)

@@ -116,6 +116,40 @@ def test_oracle_assembly_and_solvers_match_reference(n, seed):
             (want["p"], want["iterations"], want["residual"], want["converged"]), pre
 
 
+def random_mask_velocities(n, seed):
+    """The random velocity field of random_mask_system (before assembly)."""
+    dims = O.Dimz(n, n, n, 1.0 / n)
+    u, v, w, p, label = O.empty_grid(dims)
+    O.solid_shell(dims, label)
+    r = np.random.default_rng(seed)
+    lab = label.reshape(n, n, n)
+    mask = r.random(lab[1:-1, 1:-1, 1:-1].shape) < 0.4
+    lab[1:-1, 1:-1, 1:-1][mask] = O.FLUID
+    r2 = np.random.default_rng(seed + 1)
+    u[:], v[:], w[:] = r2.normal(size=u.size), r2.normal(size=v.size), r2.normal(size=w.size)
+    O.enforce(dims, label, u, v, w)
+    return dims, u, v, w, label
+
+
+@pytest.mark.parametrize("n,seed", [(8, 7), (8, 14), (12, 300)])
+def test_oracle_divergence_matches_reference(n, seed):
+    """orc_divergence_field == flipsim.grid.divergence_field (grid.py:147-156)."""
+    from golden_util import digest
+    dims, u, v, w, _ = random_mask_velocities(n, seed)
+    assert digest(O.divergence_field(dims, u, v, w)) == KERN[f"divergence_{n}_seed{seed}"]
+
+
+def test_oracle_divergence_after_steps_matches_reference():
+    from golden_util import digest
+    spec = O.Spec(name="dam-break", res=20, solver="pcg")
+    st = O.make_scene(spec, rng_seed=6)
+    for _ in range(2):
+        O.step(st, spec)
+    g = KERN["divergence_dam_break_20_seed6_step2"]
+    assert digest(st.u) == g["u"]
+    assert digest(O.divergence_field(st.dims, st.u, st.v, st.w)) == g["grid"]
+
+
 @pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 127, 128, 129, 1000, 8193, 100003, 1_000_001])
 def test_pairwise_sum_is_numpy_add_reduce(n):
     rng = np.random.default_rng(n)
@@ -150,7 +184,7 @@ def test_threads_do_not_change_oracle_results():
 
 @pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src/flipsim"),
                     reason="reference sources only exist in the build container")
-def test_oracle_equals_live_reference_64cubed():
+def test_oracle_equals_live_reference_40cubed():
     import ref_loader
     ref_loader.load()
     from flipsim import sim as RS
@@ -165,3 +199,29 @@ def test_oracle_equals_live_reference_64cubed():
     for a, b in zip(rs.particles.arrays(), os_.parts):
         assert a.tobytes() == b.tobytes()
     assert rs.grid.p.tobytes() == os_.p.tobytes()
+
+
+def test_oracle_rk2_is_midpoint_through_the_grid():
+    """orc_advect_rk2 (extension) against a numpy restatement on a random
+    grid: k1 = sample(p), m = p + k1*(dt/2), k2 = sample(m), p' = clamp(p + k2*dt)."""
+    dims = O.Dimz(6, 5, 7, 1.0 / 8.0)
+    rng = np.random.default_rng(4)
+    u = rng.normal(size=7 * 5 * 7)
+    v = rng.normal(size=6 * 6 * 7)
+    w = rng.normal(size=6 * 5 * 8)
+    n = 300
+    P = [rng.random(n) * (m / 8.0) for m in (6, 5, 7)] + [np.zeros(n)] * 3
+    lo, hi, dt, skin = np.array([0.125] * 3), np.array([0.625, 0.5, 0.75]), 0.05, 1e-4
+    k1 = O.sample_velocity_many(dims, u, v, w, *P[:3])
+    m = [P[a] + k1[a] * (0.5 * dt) for a in range(3)]
+    k2 = O.sample_velocity_many(dims, u, v, w, *m)
+    want = []
+    for a in range(3):
+        q = P[a] + k2[a] * dt
+        q = np.where(q <= lo[a], lo[a] + skin, np.where(q >= hi[a], hi[a] - skin, q))
+        want.append(q)
+    got = [a.copy() for a in P[:3]]
+    O.lib().orc_advect_rk2(O.C.byref(dims.c()), O._p(u), O._p(v), O._p(w), n, O._p(got[0]),
+                           O._p(got[1]), O._p(got[2]), dt, O._p(lo), O._p(hi), skin)
+    for a in range(3):
+        assert got[a].tobytes() == want[a].tobytes()
