@@ -222,6 +222,48 @@ int flip_set_slab(flip_ctx *ctx, int64_t k0, int64_t k1);
  * int32 buffer of n entries. */
 int flip_particle_cells(flip_ctx *ctx, int32_t *cells_dev);
 
+/* ---- z-slab decomposition driven from inside the step ----
+ * Rank r of `world` owns the cell planes [plane_start[r], plane_start[r+1])
+ * and the particles in them.  Every stage then runs on the rank's share
+ * (particles: its own; faces/cells/rows: its planes), and the step calls
+ * back into the host transport for each exchange (one NCCL/gloo collective
+ * per call; device pointers; `stream` is the ctx stream the data is ordered
+ * on).  Exchanges per step: dt MAX allreduce, particle migration
+ * (all-to-all), the label planes (all-gather; the sealed-region labelling
+ * is global), one ghost particle plane per neighbour, 1-plane face halos
+ * (after P2G, gradient, each extrapolation layer and the final enforce),
+ * per solver iteration a 1-plane row halo, MAX allreduces and the pairwise
+ * dot's boundary/partial all-gathers (bit-exact numpy tree), plus an
+ * all-gather of r per MIC(0) application (the substitution is a global
+ * recurrence: replicated on every rank).  The results are bit-identical
+ * to one GPU.  Callbacks return 0 on success. */
+#define FLIP_OP_MAX 0   /* int64 max (also non-negative doubles as bits) */
+#define FLIP_OP_MIN 1   /* int64 min */
+#define FLIP_OP_SUM 2   /* int64 sum */
+typedef struct {
+    void *user;
+    /* bytes to rank-1 / rank+1 and from rank-1 / rank+1 (sizes agree
+     * pairwise; 0 at the ends) */
+    int (*neighbors)(void *user, void *stream, const void *send_lo, int64_t nsend_lo,
+                     const void *send_hi, int64_t nsend_hi, void *recv_lo, int64_t nrecv_lo,
+                     void *recv_hi, int64_t nrecv_hi);
+    /* in place over n int64 on the device */
+    int (*allreduce)(void *user, void *stream, int64_t *buf, int64_t n, int32_t op);
+    /* in place: rank q's bytes are buf[offsets[q], offsets[q+1]); on return
+     * every rank holds all of them (offsets: host array of world+1) */
+    int (*allgatherv)(void *user, void *stream, void *buf, const int64_t *offsets);
+    /* send[sum send_bytes[<q]...] goes to rank q; recv grouped by source
+     * rank in rank order (host arrays of world byte counts) */
+    int (*alltoallv)(void *user, void *stream, const void *send, const int64_t *send_bytes,
+                     void *recv, const int64_t *recv_bytes);
+} flip_comm;
+/* Enter slab mode (comm copied; NULL comm or world 1 leaves it).  The
+ * particles must already be restricted to the rank's planes. */
+int flip_set_slab_comm(flip_ctx *ctx, int32_t rank, int32_t world, const int64_t *plane_start,
+                       const flip_comm *comm);
+/* Bytes exchanged by this ctx since the last call (then reset). */
+int flip_slab_bytes(flip_ctx *ctx, int64_t *sent, int64_t *calls);
+
 /* Diagnostics: divergence_field (grid.py:147-156) of the current grid into
  * host div[ncells]; total_energy sums (sim.py:303-315) with numpy pairwise
  * order: ke2 = sum(vx^2+vy^2+vz^2), pe = sum(py - floor_y). */

@@ -141,6 +141,8 @@ _SIGNATURES = {
     "flip_get_dev_ptrs": (C.c_int, [_vp, C.POINTER(DevPtrs)]),
     "flip_set_particle_count": (C.c_int, [_vp, C.c_int64]),
     "flip_reserve_particles": (C.c_int, [_vp, C.c_int64]),
+    "flip_set_slab_comm": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "flip_slab_bytes": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "flip_last_error_cell": (C.c_int64, []),
     "flip_set_slab": (C.c_int, [_vp, C.c_int64, C.c_int64]),
     "flip_particle_cells": (C.c_int, [_vp, _vp]),

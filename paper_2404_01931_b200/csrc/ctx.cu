@@ -123,10 +123,55 @@ static int dalloc(T **p, int64_t n) {
     return 0;
 }
 
+// Reallocate every particle-sized buffer for `cap` particles plus `front`
+// entries before index 0 (the slab ghost plane below, slab.cu).  The live
+// particles [0, n) are kept; the scratch buffers (Q, radix keys/values,
+// histograms) are simply reallocated.
+int flip::realloc_particles(Ctx &c, int64_t cap, int64_t front) {
+    const int64_t lim = ((int64_t)1 << 31) - 1;
+    if (cap + front > lim) {
+        set_error("particle count exceeds the int32 indexing limit of one device");
+        return FLIP_E_CAPACITY;
+    }
+    FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
+    for (int a = 0; a < 6; a++) {
+        double *np_ = nullptr;
+        if (int rc = dalloc(&np_, cap + front)) return rc;
+        if (c.n > 0)
+            FLIP_CUDA_OK(cudaMemcpyAsync(np_ + front, c.P.a[a], sizeof(double) * c.n,
+                                         cudaMemcpyDeviceToDevice, c.st));
+        FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
+        if (c.P.a[a]) cudaFree(c.P.a[a] - c.pfront);
+        c.P.a[a] = np_ + front;
+        if (c.Q.a[a]) cudaFree(c.Q.a[a] - c.pfront);
+        c.Q.a[a] = nullptr;
+        if (int rc = dalloc(&np_, cap + front)) return rc;
+        c.Q.a[a] = np_ + front;
+    }
+    if (cap != c.cap) {
+        int **ints[4] = {&c.keys0, &c.keys1, &c.vals0, &c.vals1};
+        for (int **q : ints) {
+            cudaFree(*q);
+            *q = nullptr;
+            if (int rc = dalloc(q, cap)) return rc;
+        }
+        cudaFree(c.hist);
+        c.hist = nullptr;
+        if (int rc = dalloc(&c.hist, radix_hist_ints(cap, c.ncells))) return rc;
+        cudaFree(c.scan_tmp);
+        c.scan_tmp = nullptr;
+        const int64_t scan_n = std::max<int64_t>(radix_hist_ints(cap, c.ncells), c.ncells + 2);
+        if (int rc = dalloc(&c.scan_tmp, scan_tmp_ints(scan_n) + 64)) return rc;
+        c.keys_valid = 0;
+    }
+    c.cap = cap;
+    c.pfront = front;
+    return 0;
+}
+
 // Grow every particle-sized buffer to hold at least n particles (the
-// reference's ParticleSet has no fixed capacity).  The live particles are
-// kept; the scratch buffers (Q, radix keys/values, histograms) are simply
-// reallocated.  Called before any launch that would exceed the capacity.
+// reference's ParticleSet has no fixed capacity).  Called before any launch
+// that would exceed the capacity.
 int flip::reserve_particles(Ctx &c, int64_t n) {
     if (n <= c.cap) return 0;
     const int64_t lim = ((int64_t)1 << 31) - 1;
@@ -134,37 +179,8 @@ int flip::reserve_particles(Ctx &c, int64_t n) {
         set_error("particle count exceeds the int32 indexing limit of one device");
         return FLIP_E_CAPACITY;
     }
-    const int64_t cap = std::min(lim, std::max(n, c.cap + c.cap / 2));
-    FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
-    for (int a = 0; a < 6; a++) {
-        double *np_ = nullptr;
-        if (int rc = dalloc(&np_, cap)) return rc;
-        if (c.n > 0)
-            FLIP_CUDA_OK(cudaMemcpyAsync(np_, c.P.a[a], sizeof(double) * c.n,
-                                         cudaMemcpyDeviceToDevice, c.st));
-        FLIP_CUDA_OK(cudaStreamSynchronize(c.st));
-        cudaFree(c.P.a[a]);
-        c.P.a[a] = np_;
-        cudaFree(c.Q.a[a]);
-        c.Q.a[a] = nullptr;
-        if (int rc = dalloc(&c.Q.a[a], cap)) return rc;
-    }
-    int **ints[4] = {&c.keys0, &c.keys1, &c.vals0, &c.vals1};
-    for (int **q : ints) {
-        cudaFree(*q);
-        *q = nullptr;
-        if (int rc = dalloc(q, cap)) return rc;
-    }
-    cudaFree(c.hist);
-    c.hist = nullptr;
-    if (int rc = dalloc(&c.hist, radix_hist_ints(cap, c.ncells))) return rc;
-    cudaFree(c.scan_tmp);
-    c.scan_tmp = nullptr;
-    const int64_t scan_n = std::max<int64_t>(radix_hist_ints(cap, c.ncells), c.ncells + 2);
-    if (int rc = dalloc(&c.scan_tmp, scan_tmp_ints(scan_n) + 64)) return rc;
-    c.cap = cap;
-    c.keys_valid = 0;
-    return 0;
+    const int64_t cap = std::min(lim - c.pfront, std::max(n, c.cap + c.cap / 2));
+    return realloc_particles(c, cap, c.pfront);
 }
 
 #define ALLOC(ptr, n)                                \
@@ -180,8 +196,12 @@ extern "C" void flip_destroy(flip_ctx *c) {
     cudaSetDevice(c->device);
     if (c->st) cudaStreamSynchronize(c->st);
     mg_free(*c);
-    void *ptrs[] = {c->P.a[0], c->P.a[1], c->P.a[2], c->P.a[3], c->P.a[4], c->P.a[5], c->Q.a[0],
-                    c->Q.a[1], c->Q.a[2], c->Q.a[3], c->Q.a[4], c->Q.a[5], c->u, c->v, c->w, c->p,
+    slab_free(*c);
+    for (int a = 0; a < 6; a++) {
+        if (c->P.a[a]) cudaFree(c->P.a[a] - c->pfront);
+        if (c->Q.a[a]) cudaFree(c->Q.a[a] - c->pfront);
+    }
+    void *ptrs[] = {c->u, c->v, c->w, c->p,
                     c->label, c->uo, c->vo, c->wo, c->ku, c->kv, c->kw, c->ku1, c->kv1, c->kw1,
                     c->count, c->offset, c->count2, c->offset2, c->nadd, c->keys0, c->keys1,
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
@@ -649,6 +669,12 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
         set_error("unknown solver or preconditioner");
         return FLIP_E_CONFIG;
     }
+    if (c->slab.on && prm->advection == FLIP_ADVECT_RK2) {
+        // the RK2 midpoint samples the grid up to 1.5 cells beyond the slab:
+        // the 1-plane halos do not cover it
+        set_error("RK2 advection is not supported with a slab decomposition");
+        return FLIP_E_CONFIG;
+    }
     int64_t launches0 = c->launches;
     bool keys_from_advect = false, force_fused = false, reseed_ran = false;
     int status = 0;
@@ -668,11 +694,15 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
         cudaEventRecord(c->ev[s], c->st);
         switch (s) {
             case FLIP_STAGE_DT:
-                stage_dt(*c, *prm);
+                if (int rc = stage_dt(*c, *prm)) return rc;
                 break;
             case FLIP_STAGE_ADVECT:
                 stage_advect(*c, *prm);
-                keys_from_advect = true;
+                if (c->slab.on) {  // particles to the rank owning their new cell
+                    if (int rc = slab_migrate(*c)) return rc;
+                } else {
+                    keys_from_advect = true;
+                }
                 break;
             case FLIP_STAGE_BIN:
                 if (keys_from_advect) stage_bin_from_keys(*c);
@@ -680,13 +710,26 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
                 break;
             case FLIP_STAGE_CLASSIFY:
                 stage_classify(*c);
+                if (c->slab.on)
+                    if (int rc = slab_labels(*c)) return rc;
                 break;
             case FLIP_STAGE_P2G:
                 force_fused = last >= FLIP_STAGE_FORCE;
+                if (c->slab.on)
+                    if (int rc = slab_ghosts(*c)) return rc;
                 stage_p2g_impl(*c, prm, force_fused ? 1 : 0);
+                if (c->slab.on) {
+                    slab_ghosts_clear(*c);
+                    if (int rc = slab_face_halo(*c, SLAB_H_GRID | SLAB_H_OLD | SLAB_H_KNOWN))
+                        return rc;
+                }
                 break;
             case FLIP_STAGE_FORCE:
-                if (!force_fused) stage_force(*c, *prm);
+                if (!force_fused) {
+                    stage_force(*c, *prm);
+                    if (c->slab.on)
+                        if (int rc = slab_face_halo(*c, SLAB_H_GRID)) return rc;
+                }
                 break;
             case FLIP_STAGE_PROJECT: {
                 int rc = stage_project(*c, *prm, rep);
@@ -699,7 +742,7 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
                     set_error("apply_gradient needs the P2G known masks (run P2G or flip_set_known)");
                     return FLIP_E_ARG;
                 }
-                stage_apply_gradient(*c, *prm);
+                if (int rc = stage_apply_gradient(*c, *prm)) return rc;
                 break;
             case FLIP_STAGE_G2P:
                 stage_g2p(*c, *prm);

@@ -49,11 +49,11 @@ __device__ __forceinline__ bool face_cells(const Dims &d, int comp, int i, int j
 // over one component; force skipped when g == 0 or apply_force == 0.
 __global__ void k_force_enforce(double *__restrict__ a, Dims d, int comp, double g,
                                 const DevScalars *__restrict__ sc, int apply_force,
-                                const uint8_t *__restrict__ label) {
+                                const uint8_t *__restrict__ label, unsigned f_lo, unsigned f_hi) {
     Lat L = lat(d, comp);
-    const unsigned n = (unsigned)L.mx * L.my * L.mz;
+    const unsigned n = f_hi;
     double inc = (apply_force && g != 0.0) ? g * sc->dt : 0.0;
-    for (unsigned f = ugtid(); f < n; f += ugstride()) {
+    for (unsigned f = f_lo + ugtid(); f < n; f += ugstride()) {
         int i, j, k;
         lat_ijk(L, f, i, j, k);
         int64_t lo, hi;
@@ -66,10 +66,14 @@ __global__ void k_force_enforce(double *__restrict__ a, Dims d, int comp, double
 void stage_force(Ctx &c, const flip_step_params &prm) {
     double *arr[3] = {c.u, c.v, c.w};
     int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
+    (void)nf;
     for (int comp = 0; comp < 3; comp++) {
-        k_force_enforce<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(arr[comp], c.d, comp,
-                                                                  prm.gravity[comp], c.sc, 1,
-                                                                  c.label);
+        int64_t lo, hi;
+        slab_face_range(c, comp, &lo, &hi);
+        k_force_enforce<<<nblocks(hi - lo), kThreads, 0, c.st>>>(arr[comp], c.d, comp,
+                                                                 prm.gravity[comp], c.sc, 1,
+                                                                 c.label, (unsigned)lo,
+                                                                 (unsigned)hi);
         c.launches++;
     }
 }
@@ -145,7 +149,8 @@ void launch_enforce(Ctx &c, double *u, double *v, double *w) {
     int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
     for (int comp = 0; comp < 3; comp++) {
         k_force_enforce<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(arr[comp], c.d, comp, 0.0, c.sc,
-                                                                  0, c.label);
+                                                                  0, c.label, 0u,
+                                                                  (unsigned)nf[comp]);
         c.launches++;
     }
 }
@@ -153,11 +158,11 @@ void launch_enforce(Ctx &c, double *u, double *v, double *w) {
 // apply_pressure_gradient (pressure.py:343-380): scale = dt / (rho*dtau).
 __global__ void k_gradient(double *__restrict__ a, Dims d, int comp, const double *__restrict__ p,
                            const uint8_t *__restrict__ label, const DevScalars *__restrict__ sc,
-                           double rho_dtau) {
+                           double rho_dtau, unsigned f_lo, unsigned f_hi) {
     Lat L = lat(d, comp);
-    const unsigned n = (unsigned)L.mx * L.my * L.mz;
+    const unsigned n = f_hi;
     double scale = sc->dt / rho_dtau;
-    for (unsigned f = ugtid(); f < n; f += ugstride()) {
+    for (unsigned f = f_lo + ugtid(); f < n; f += ugstride()) {
         int i, j, k;
         lat_ijk(L, f, i, j, k);
         int64_t lo, hi;
@@ -176,10 +181,11 @@ __global__ void k_gradient(double *__restrict__ a, Dims d, int comp, const doubl
 // kin is set and writes only where it is not, so the update is in place.
 // Accumulation order: 0 + v(k+1) + v(k-1) + v(j+1) + v(j-1) + v(i+1) + v(i-1).
 __global__ void k_extrap_layer(double *__restrict__ A, double *__restrict__ B, Lat L,
-                               const uint8_t *__restrict__ kin, uint8_t *__restrict__ kout) {
-    const unsigned n = (unsigned)L.mx * L.my * L.mz;
+                               const uint8_t *__restrict__ kin, uint8_t *__restrict__ kout,
+                               unsigned f_lo, unsigned f_hi) {
+    const unsigned n = f_hi;
     const int64_t sy = L.mx, sz = (int64_t)L.mx * L.my;
-    for (unsigned f = ugtid(); f < n; f += ugstride()) {
+    for (unsigned f = f_lo + ugtid(); f < n; f += ugstride()) {
         if (kin[f]) {
             kout[f] = 1;
             continue;
@@ -208,29 +214,45 @@ __global__ void k_extrap_layer(double *__restrict__ A, double *__restrict__ B, L
 }
 
 // pressure_field (pressure.py:49-53) is written by stage_project.
-void stage_apply_gradient(Ctx &c, const flip_step_params &prm) {
+// Slab mode: every kernel covers the own face planes, and the face planes
+// next to the slab are refreshed from the neighbours between the passes that
+// read them (gradient -> layer 0 -> layer 1 -> ... -> enforce -> G2P).
+int stage_apply_gradient(Ctx &c, const flip_step_params &prm) {
     double *g[3] = {c.u, c.v, c.w}, *o[3] = {c.uo, c.vo, c.wo};
-    uint8_t *k0[3] = {c.ku, c.kv, c.kw}, *k1[3] = {c.ku1, c.kv1, c.kw1};
-    int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
+    uint8_t *k0[3] = {c.ku, c.kv, c.kw};
     // scratch mask pairs: layer l reads (l == 0 ? P2G mask : s[(l-1)&1]), writes s[l&1]
     uint8_t *s0[3] = {c.ku1, c.kv1, c.kw1};
     uint8_t *s1[3] = {c.ku1 + c.nfu, c.kv1 + c.nfv, c.kw1 + c.nfw};
-    (void)k1;
+    int64_t lo[3], hi[3];
+    for (int comp = 0; comp < 3; comp++) slab_face_range(c, comp, &lo[comp], &hi[comp]);
     for (int comp = 0; comp < 3; comp++) {
-        k_gradient<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(g[comp], c.d, comp, c.p, c.label, c.sc,
-                                                             prm.rho_dtau_h);
+        k_gradient<<<nblocks(hi[comp] - lo[comp]), kThreads, 0, c.st>>>(
+            g[comp], c.d, comp, c.p, c.label, c.sc, prm.rho_dtau_h, (unsigned)lo[comp],
+            (unsigned)hi[comp]);
         c.launches++;
     }
-    for (int comp = 0; comp < 3; comp++) {
-        Lat L = lat(c.d, comp);
-        for (int l = 0; l < prm.extrapolation_layers; l++) {
+    const int layers = prm.extrapolation_layers;
+    if (c.slab.on && layers > 0)
+        if (int rc = slab_face_halo(c, SLAB_H_GRID)) return rc;
+    for (int l = 0; l < layers; l++) {
+        for (int comp = 0; comp < 3; comp++) {
+            Lat L = lat(c.d, comp);
             const uint8_t *kin = l == 0 ? k0[comp] : ((l - 1) & 1 ? s1[comp] : s0[comp]);
             uint8_t *kout = (l & 1) ? s1[comp] : s0[comp];
-            k_extrap_layer<<<nblocks(nf[comp]), kThreads, 0, c.st>>>(g[comp], o[comp], L, kin, kout);
+            k_extrap_layer<<<nblocks(hi[comp] - lo[comp]), kThreads, 0, c.st>>>(
+                g[comp], o[comp], L, kin, kout, (unsigned)lo[comp], (unsigned)hi[comp]);
             c.launches++;
         }
+        if (c.slab.on && l + 1 < layers)
+            if (int rc = slab_face_halo(c, SLAB_H_GRID | SLAB_H_OLD |
+                                               ((l & 1) ? SLAB_H_SCRATCH1 : SLAB_H_SCRATCH0)))
+                return rc;
     }
     launch_enforce(c, c.u, c.v, c.w);
+    // G2P and reseed sample both grids one plane beyond the slab
+    if (c.slab.on)
+        if (int rc = slab_face_halo(c, SLAB_H_GRID | SLAB_H_OLD)) return rc;
+    return 0;
 }
 
 // divergence_field (grid.py:147-156)

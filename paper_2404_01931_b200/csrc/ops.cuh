@@ -1,6 +1,7 @@
 // ops.cuh — device context and kernel launcher declarations for libflipb200.
 #pragma once
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -43,12 +44,40 @@ struct Probe {
     int64_t launches = 0;
 };
 
+// z-slab decomposition state (flip_set_slab_comm, slab.cu).  All arrays
+// keep their full-grid size and global indexing; a rank only computes its
+// own planes / rows / particles and exchanges the boundary planes.
+struct Slab {
+    bool on = false;
+    int rank = 0, world = 1;
+    std::vector<int64_t> kstart;   // world + 1 plane starts
+    int *kstart_dev = nullptr;     // same, on the device (int)
+    flip_comm comm{};
+    int64_t k0 = 0, k1 = 0;        // own cell planes [k0, k1)
+    int64_t g_lo = 0, g_hi = 0;    // ghost particles placed for the current P2G
+    // pressure rows (global numbering; set by stage_project)
+    std::vector<int64_t> rstart;   // world + 1: first global row of each rank
+    int64_t R0 = 0, R1 = 0;        // own rows
+    int64_t Rlo = 0, Rhi = 0;      // own rows plus the rows of planes k0-1 and k1
+    int64_t R0f = 0, R1l = 0;      // end of the rows of plane k0 / start of plane k1-1
+    // exchange staging and migration scratch (grown on demand)
+    char *xbuf = nullptr;
+    size_t xcap = 0;
+    int *mig = nullptr;            // 5 int arrays of mig_cap + histogram
+    int64_t mig_cap = 0;
+    int64_t *cnt_dev = nullptr;    // world x world counts / small scalars
+    double *dotbuf = nullptr;      // distributed dot scratch (pressure.cu)
+    size_t dotcap = 0;
+    int64_t bytes = 0, calls = 0;  // exchange accounting (flip_slab_bytes)
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;
     Dims d{};
     int64_t ncells = 0, nfu = 0, nfv = 0, nfw = 0;
-    int64_t cap = 0;        // particle capacity
+    int64_t cap = 0;        // particle capacity (entries from P.a[a][0])
+    int64_t pfront = 0;     // extra entries before P.a[a][0] (slab ghost plane below)
     int64_t n = 0;          // particle count (host mirror)
     int64_t slab_c0 = 0, slab_c1 = -1;  // reseed cell range (flip_set_slab); -1: all
     void *f32_buf = nullptr;           // snapshot staging (flip_*_particles_f32)
@@ -101,6 +130,7 @@ struct Ctx {
     Probe probe;
     int known_valid = 0;
     int keys_valid = 0;   // keys_sorted matches the current binned particles
+    Slab slab;
 };
 
 // ---- sort / scan ----
@@ -113,7 +143,7 @@ int radix_sort_cells(int *k0, int *k1, int *v0, int *v1, int64_t n, int64_t ncel
                      int **perm_out, int64_t *launches);
 
 // ---- stage launchers (ctx-based, stream-ordered, no host sync) ----
-void stage_dt(Ctx &c, const flip_step_params &prm);
+int stage_dt(Ctx &c, const flip_step_params &prm);
 void stage_advect(Ctx &c, const flip_step_params &prm);
 void stage_bin(Ctx &c);                                // keys + count + scan + sort + gather
 void stage_bin_from_keys(Ctx &c);                      // same, keys/count already computed
@@ -122,7 +152,7 @@ void stage_p2g(Ctx &c, const flip_step_params &prm);   // + grid_old copy, known
 void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force);
 void stage_force(Ctx &c, const flip_step_params &prm); // body force + enforce
 int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep);  // syncs
-void stage_apply_gradient(Ctx &c, const flip_step_params &prm);
+int stage_apply_gradient(Ctx &c, const flip_step_params &prm);
 void stage_g2p(Ctx &c, const flip_step_params &prm);
 int stage_reseed(Ctx &c, const flip_step_params &prm);
 void launch_particle_cells(Ctx &c, int *out);
@@ -139,6 +169,26 @@ int seed_regions(Ctx &c, int nreg, const flip_region *regs, uint64_t seed);
 int reserve_particles(Ctx &c, int64_t n);
 void launch_divergence(Ctx &c, double *div_dev);
 void launch_enforce(Ctx &c, double *u, double *v, double *w);
+
+// ---- slab decomposition (slab.cu) ----
+int slab_neighbors(Ctx &c, const void *slo, int64_t nslo, const void *shi, int64_t nshi,
+                   void *rlo, int64_t nrlo, void *rhi, int64_t nrhi);
+int slab_allreduce(Ctx &c, int64_t *buf, int64_t n, int op);
+int slab_allgatherv(Ctx &c, void *buf, const int64_t *offsets);
+char *slab_xbuf(Ctx &c, size_t bytes);
+int slab_migrate(Ctx &c);                   // after ADVECT: particles to their owners
+int slab_labels(Ctx &c);                    // after CLASSIFY: full label array
+int slab_ghosts(Ctx &c);                    // before P2G: neighbour particle planes
+void slab_ghosts_clear(Ctx &c);             // after P2G
+int slab_face_halo(Ctx &c, int what);       // 1-plane face halos (SLAB_H_* bits)
+int slab_row_halo(Ctx &c, double *vec);     // 1-plane row halo of a row vector
+int slab_rows(Ctx &c);                      // global row ranges (after the row scan)
+int slab_free(Ctx &c);
+// own face range of lattice comp: [lo, hi) flat indices
+void slab_face_range(const Ctx &c, int comp, int64_t *lo, int64_t *hi);
+enum { SLAB_H_GRID = 1, SLAB_H_OLD = 2, SLAB_H_KNOWN = 4, SLAB_H_SCRATCH0 = 8, SLAB_H_SCRATCH1 = 16 };
+// distributed numpy-pairwise dot over the own rows (pressure.cu)
+int realloc_particles(Ctx &c, int64_t cap, int64_t front);
 
 // ---- kernel-level helpers shared with the plugin API ----
 void launch_sample_many(const Dims &d, const double *u, const double *v, const double *w,

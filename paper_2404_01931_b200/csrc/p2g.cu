@@ -60,15 +60,17 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
       const double *__restrict__ pz, const double *__restrict__ vel,
       const int *__restrict__ offset, const int *__restrict__ count, P2GOut out,
       const uint8_t *__restrict__ label, const DevScalars *__restrict__ sc, double g,
-      int fuse_force) {
+      int fuse_force, unsigned f_lo, unsigned f_hi) {
     FaceLattice L = lattice(d, comp);
-    // 32-bit index math: flip_create rejects grids with >= 2^31 faces
-    const unsigned nf = (unsigned)L.fnx * L.fny * L.fnz;
+    // 32-bit index math: flip_create rejects grids with >= 2^31 faces;
+    // [f_lo, f_hi): all faces, or the own planes of a slab
+    const unsigned nf = f_hi;
     int nx = d.nx, ny = d.ny, nz = d.nz;
     const int sxy = nx * ny;
     double gdt = 0.0;
     if (fuse_force && g != 0.0) gdt = g * sc->dt;
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
+    for (unsigned f = f_lo + blockIdx.x * blockDim.x + threadIdx.x; f < nf;
+         f += gridDim.x * blockDim.x) {
         const unsigned fq = f / (unsigned)L.fnx;
         int fi = (int)(f - fq * (unsigned)L.fnx);
         int fj = (int)(fq % (unsigned)L.fny);
@@ -146,12 +148,15 @@ void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force) {
     double *grid[3] = {c.u, c.v, c.w}, *old[3] = {c.uo, c.vo, c.wo};
     uint8_t *known[3] = {c.ku, c.kv, c.kw};
     int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
+    (void)nf;
     for (int comp = 0; comp < 3; comp++) {
         P2GOut o{grid[comp], old[comp], known[comp], nullptr};
         double g = prm ? prm->gravity[comp] : 0.0;
-        k_p2g<true><<<nblocks(nf[comp], kThreads, (int64_t)1 << 30), kThreads, 0, c.st>>>(
+        int64_t f_lo, f_hi;
+        slab_face_range(c, comp, &f_lo, &f_hi);
+        k_p2g<true><<<nblocks(f_hi - f_lo, kThreads, (int64_t)1 << 30), kThreads, 0, c.st>>>(
             c.d, comp, c.P.a[0], c.P.a[1], c.P.a[2], c.P.a[3 + comp], c.offset, nullptr, o,
-            c.label, c.sc, g, fuse_force);
+            c.label, c.sc, g, fuse_force, (unsigned)f_lo, (unsigned)f_hi);
         c.launches++;
     }
     c.known_valid = 1;
@@ -166,7 +171,7 @@ void launch_p2g_component(const Dims &d, int comp, const double *vel, const doub
     int64_t nf = (int64_t)L.fnx * L.fny * L.fnz;
     P2GOut o{out, nullptr, nullptr, den};
     k_p2g<false><<<nblocks(nf, kThreads, (int64_t)1 << 30), kThreads, 0, st>>>(
-        d, comp, px, py, pz, vel, offset, count, o, nullptr, nullptr, 0.0, 0);
+        d, comp, px, py, pz, vel, offset, count, o, nullptr, nullptr, 0.0, 0, 0u, (unsigned)nf);
 }
 
 }  // namespace flip

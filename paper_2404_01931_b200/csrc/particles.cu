@@ -29,14 +29,19 @@ __global__ void k_dt_final(DevScalars *sc, double alpha_dtau, double dt_max) {
     sc->dt = dt;
 }
 
-void stage_dt(Ctx &c, const flip_step_params &prm) {
+int stage_dt(Ctx &c, const flip_step_params &prm) {
     cudaMemsetAsync(&c.sc->s2max_bits, 0, sizeof(unsigned long long), c.st);
     if (c.n > 0) {
         k_maxv2<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, &c.sc->s2max_bits);
         c.launches++;
     }
+    // slab mode: max |v|^2 over every rank (a non-negative double: its bits
+    // order like the value), so dt is the 1-GPU dt bit for bit
+    if (c.slab.on)
+        if (int rc = slab_allreduce(c, (int64_t *)&c.sc->s2max_bits, 1, FLIP_OP_MAX)) return rc;
     k_dt_final<<<1, 1, 0, c.st>>>(c.sc, prm.alpha_dtau_h, prm.dt_max);
     c.launches++;
+    return 0;
 }
 
 // ---------------------------------------------------------------- advect --
@@ -198,7 +203,9 @@ __global__ void k_classify(uint8_t *__restrict__ label, const int *__restrict__ 
 }
 
 void stage_classify(Ctx &c) {
-    k_classify<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.count, c.ncells);
+    // slab mode: the own cells only (the other planes arrive by slab_labels)
+    const int64_t c0 = c.slab.on ? c.slab_c0 : 0, c1 = c.slab.on ? c.slab_c1 : c.ncells;
+    k_classify<<<nblocks(c1 - c0), kThreads, 0, c.st>>>(c.label + c0, c.count + c0, c1 - c0);
     c.launches++;
 }
 

@@ -190,12 +190,16 @@ __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
                                 const double *__restrict__ u, const double *__restrict__ v,
                                 const double *__restrict__ w, int *__restrict__ nbr, int64_t ldn,
                                 double *__restrict__ diag, double *__restrict__ rhs,
-                                unsigned long long *rhsmax, DevScalars *scw) {
-    int n = sc->nrows;
+                                unsigned long long *rhsmax, DevScalars *scw, int64_t a_lo,
+                                int64_t a_hi, int64_t rhs_lo, int64_t rhs_hi) {
+    // rows [a_lo, a_hi) get their structure (a_hi < 0: all rows); rhs only
+    // on [rhs_lo, rhs_hi) (a slab's own rows; rhs_hi < 0: all), 0 elsewhere
+    const int64_t n = a_hi < 0 ? (int64_t)sc->nrows : a_hi;
+    if (rhs_hi < 0) rhs_hi = n;
     int64_t sxy = (int64_t)d.nx * d.ny;
     double m = 0.0;
     int lo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, hi[3] = {-1, -1, -1};
-    for (int64_t r = gtid(); r < n; r += gstride()) {
+    for (int64_t r = a_lo + gtid(); r < n; r += gstride()) {
         int64_t c = cell_of_row[r];
         int i, j, k;
         cell_ijk(d, c, i, j, k);
@@ -216,19 +220,23 @@ __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
             nbr[q * ldn + r] = nb;
         }
         diag[r] = (double)ns;
-        int64_t fu0 = i + (int64_t)j * (d.nx + 1) + (int64_t)k * (d.nx + 1) * d.ny;
-        int64_t fv0 = i + (int64_t)j * d.nx + (int64_t)k * d.nx * (d.ny + 1);
-        int64_t fw0 = c;
-        double u0 = nl[0] == SOLID ? 0.0 : u[fu0];
-        double u1 = nl[1] == SOLID ? 0.0 : u[fu0 + 1];
-        double v0 = nl[2] == SOLID ? 0.0 : v[fv0];
-        double v1 = nl[3] == SOLID ? 0.0 : v[fv0 + d.nx];
-        double w0 = nl[4] == SOLID ? 0.0 : w[fw0];
-        double w1 = nl[5] == SOLID ? 0.0 : w[fw0 + sxy];
-        double div = (((((u1 - u0) + v1) - v0) + w1) - w0) / d.dtau;
-        double rh = -div;
-        rhs[r] = rh;
-        m = fmax(m, fabs(rh));
+        if (r >= rhs_lo && r < rhs_hi) {
+            int64_t fu0 = i + (int64_t)j * (d.nx + 1) + (int64_t)k * (d.nx + 1) * d.ny;
+            int64_t fv0 = i + (int64_t)j * d.nx + (int64_t)k * d.nx * (d.ny + 1);
+            int64_t fw0 = c;
+            double u0 = nl[0] == SOLID ? 0.0 : u[fu0];
+            double u1 = nl[1] == SOLID ? 0.0 : u[fu0 + 1];
+            double v0 = nl[2] == SOLID ? 0.0 : v[fv0];
+            double v1 = nl[3] == SOLID ? 0.0 : v[fv0 + d.nx];
+            double w0 = nl[4] == SOLID ? 0.0 : w[fw0];
+            double w1 = nl[5] == SOLID ? 0.0 : w[fw0 + sxy];
+            double div = (((((u1 - u0) + v1) - v0) + w1) - w0) / d.dtau;
+            double rh = -div;
+            rhs[r] = rh;
+            m = fmax(m, fabs(rh));
+        } else {
+            rhs[r] = 0.0;
+        }
         lo[0] = min(lo[0], i); hi[0] = max(hi[0], i);
         lo[1] = min(lo[1], j); hi[1] = max(hi[1], j);
         lo[2] = min(lo[2], k); hi[2] = max(hi[2], k);
@@ -561,6 +569,245 @@ void launch_pairwise_dot(const double *a, const double *b, int64_t n, double *tm
     launch_dot(a, b, n, tmp, out_dev, EPI_STORE, nullptr, st, launches);
 }
 
+// ============================================ distributed pairwise dot (slab)
+// The same numpy tree over the GLOBAL row vector (length n), with rank r
+// holding rows [R0, R1).  Rank r evaluates the cut-level nodes that START in
+// its rows (a node reaching past R1 reads the next ranks' leading products,
+// all-gathered), reduces them to the maximal aligned blocks of the perfect
+// tree above the cut, and every rank merges all ranks' blocks in index
+// order: each internal node is still left + right, so the sum is bit-
+// identical to the one-GPU dot (and to np.add.reduce).
+struct DotPlan {
+    int64_t n = -1;      // global rows the plan was built for
+    int cut = 0;
+    int64_t na = 0, nb = 0;  // my nodes
+    int64_t X = 0;       // longest cut-level node
+    int64_t pre_len = 0; // my leading products published (min(X, own rows))
+    std::vector<int64_t> pre_off;  // bytes, world + 1
+    int64_t ext_off = 0; // element offset of rank r+1's prefix in the gather buffer
+};
+
+static void node_span(int64_t n, int cut, int64_t node, int64_t *s, int64_t *len) {
+    int64_t s0 = 0, l = n;
+    for (int lvl = cut - 1; lvl >= 0; lvl--) {
+        int64_t n2 = l / 2;
+        n2 -= n2 % 8;
+        if ((node >> lvl) & 1) {
+            s0 += n2;
+            l -= n2;
+        } else {
+            l = n2;
+        }
+    }
+    *s = s0;
+    *len = l;
+}
+
+static int64_t first_node_at_or_after(int64_t n, int cut, int64_t row) {
+    int64_t lo = 0, hi = (int64_t)1 << cut;  // first node with start >= row
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2, s, l;
+        node_span(n, cut, mid, &s, &l);
+        if (s >= row) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+template <class LD>
+struct LdExt {  // rows >= R1 come from the gathered leading products
+    LD ld;
+    int64_t R1;
+    const double *ext;
+    __device__ __forceinline__ double operator()(int64_t i) const {
+        return i < R1 ? ld(i) : ext[i - R1];
+    }
+};
+
+template <class LD>
+__global__ void k_dotd_prefix(LD ld, int64_t R0, int64_t m, double *__restrict__ out,
+                              const DevScalars *sc, int skip) {
+    if (skip && sc->done) return;
+    for (int64_t i = gtid(); i < m; i += gstride()) out[i] = ld(R0 + i);
+}
+
+template <class LD>
+__global__ void k_dotd_nodes(LD ld, int64_t n, int cut, int64_t na, int64_t nb,
+                             double *__restrict__ out, const DevScalars *sc, int skip) {
+    if (skip && sc->done) return;
+    const int g = threadIdx.x & 7;
+    const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 3;
+    for (int64_t node = na + (gtid() >> 3); node < nb; node += groups) {
+        int64_t s0 = 0, len = n;
+        for (int lvl = cut - 1; lvl >= 0; lvl--) {
+            int64_t n2 = pw_split(len);
+            if ((node >> lvl) & 1) {
+                s0 += n2;
+                len -= n2;
+            } else {
+                len = n2;
+            }
+        }
+        const double v = pw_node8<2>(ld, s0, len, g);
+        if (g == 0) out[node - na] = v;
+    }
+}
+
+// In place: the perfect tree inside every aligned block [g, g + 2^k) that
+// lies within [na, nb); then the maximal blocks, in order, as (level, index,
+// value) entries (entry 0 holds the count).
+__global__ void __launch_bounds__(1024) k_dotd_canon(double *__restrict__ v, int64_t na, int64_t nb,
+                                                     double *__restrict__ ent, const DevScalars *sc,
+                                                     int skip) {
+    if (skip && sc->done) return;
+    const int64_t cnt = nb - na;
+    for (int64_t st = 1; st < cnt; st <<= 1) {
+        for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int64_t g = na + i;
+            if (g % (2 * st) == 0 && g + 2 * st <= nb) v[i] = v[i] + v[i + st];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        int k = 0;
+        int64_t g = na;
+        while (g < nb) {
+            int lvl = 0;
+            while (((g >> lvl) & 1) == 0 && g + ((int64_t)2 << lvl) <= nb && lvl < 62) lvl++;
+            // largest aligned block at g inside [g, nb)
+            while (g + ((int64_t)1 << lvl) > nb) lvl--;
+            const long long key = ((long long)lvl << 56) | (long long)(g >> lvl);
+            ent[2 + 2 * k] = __longlong_as_double(key);
+            ent[3 + 2 * k] = v[g - na];
+            k++;
+            g += (int64_t)1 << lvl;
+        }
+        ent[0] = (double)k;
+    }
+}
+
+constexpr int kDotEnt = 2 + 2 * 64;  // doubles per rank slot: header + up to 64 blocks
+
+__global__ void k_dotd_merge(const double *__restrict__ ent, int world, int epi, double *out,
+                             DevScalars *sc, int skip) {
+    if (skip && sc->done) return;
+    long long lv[128], ix[128];
+    double val[128];
+    int sp = 0;
+    for (int q = 0; q < world; q++) {
+        const double *e = ent + (int64_t)q * kDotEnt;
+        const int k = (int)e[0];
+        for (int t = 0; t < k; t++) {
+            const long long key = __double_as_longlong(e[2 + 2 * t]);
+            lv[sp] = key >> 56;
+            ix[sp] = key & ((1ll << 56) - 1);
+            val[sp] = e[3 + 2 * t];
+            sp++;
+            while (sp >= 2 && lv[sp - 1] == lv[sp - 2] && (ix[sp - 2] & 1) == 0 &&
+                   ix[sp - 1] == ix[sp - 2] + 1) {
+                val[sp - 2] = val[sp - 2] + val[sp - 1];
+                lv[sp - 2] += 1;
+                ix[sp - 2] >>= 1;
+                sp--;
+            }
+        }
+    }
+    dot_epilogue(sp == 1 ? val[0] : __longlong_as_double(0x7ff8000000000001ll), epi, out, sc);
+}
+
+struct SlabDot {
+    Ctx *c;
+    DotPlan plan;
+    double *nodes = nullptr;   // node sums (device)
+    double *pre = nullptr;     // gathered leading products
+    double *ent = nullptr;     // gathered canonical blocks
+};
+
+static int slabdot_plan(SlabDot &D, int64_t n) {
+    Ctx &c = *D.c;
+    Slab &S = c.slab;
+    DotPlan &P = D.plan;
+    if (P.n == n) return 0;
+    P.n = n;
+    P.cut = pw_cut(n > 0 ? n : 1);
+    // longest node at the cut level
+    {
+        std::vector<int64_t> sizes{n};
+        for (int l = 0; l < P.cut; l++) {
+            std::vector<int64_t> nx;
+            for (int64_t sz : sizes) {
+                int64_t n2 = sz / 2 - (sz / 2) % 8;
+                nx.push_back(n2);
+                nx.push_back(sz - n2);
+            }
+            std::sort(nx.begin(), nx.end());
+            nx.erase(std::unique(nx.begin(), nx.end()), nx.end());
+            sizes.swap(nx);
+        }
+        P.X = sizes.empty() ? 0 : sizes.back();
+    }
+    P.na = first_node_at_or_after(n, P.cut, S.R0);
+    P.nb = first_node_at_or_after(n, P.cut, S.R1);
+    if (S.R1 >= n) P.nb = (int64_t)1 << P.cut;  // the last rank owns the tail
+    if (S.R0 >= n) P.na = P.nb;
+    P.pre_off.assign(S.world + 1, 0);
+    for (int q = 0; q < S.world; q++) {
+        const int64_t rows = S.rstart[q + 1] - S.rstart[q];
+        P.pre_off[q + 1] = P.pre_off[q] + 8 * std::min(P.X, rows);
+    }
+    P.pre_len = (P.pre_off[S.rank + 1] - P.pre_off[S.rank]) / 8;
+    P.ext_off = P.pre_off[std::min(S.rank + 1, S.world)] / 8;
+    size_t need = 8 * ((size_t)(P.nb - P.na) + (size_t)(P.pre_off[S.world] / 8) +
+                       (size_t)S.world * kDotEnt + 64);
+    if (need > S.dotcap) {
+        cudaStreamSynchronize(c.st);
+        cudaFree(S.dotbuf);
+        S.dotbuf = nullptr;
+        S.dotcap = 0;
+        FLIP_CUDA_OK(cudaMalloc(&S.dotbuf, need));
+        S.dotcap = need;
+    }
+    D.nodes = S.dotbuf;
+    D.pre = D.nodes + (P.nb - P.na) + 8;
+    D.ent = D.pre + P.pre_off[S.world] / 8 + 8;
+    return 0;
+}
+
+template <class LD>
+static int launch_dot_slab(SlabDot &D, const LD &ld, int64_t n, double *out_dev, int epi,
+                           DevScalars *sc, cudaStream_t st, int64_t *launches) {
+    Ctx &c = *D.c;
+    Slab &S = c.slab;
+    if (int rc = slabdot_plan(D, n)) return rc;
+    const DotPlan &P = D.plan;
+    const int skip = (epi == EPI_CURV || epi == EPI_SIGMA_NEW) ? 1 : 0;
+    // (1) leading products of every rank
+    if (P.pre_len > 0) {
+        k_dotd_prefix<<<nblocks(P.pre_len), kThreads, 0, st>>>(
+            ld, S.R0, P.pre_len, D.pre + P.pre_off[S.rank] / 8, sc, skip);
+        (*launches)++;
+    }
+    if (int rc = slab_allgatherv(c, D.pre, P.pre_off.data())) return rc;
+    // (2) my nodes, (3) my maximal blocks
+    const int64_t m = P.nb - P.na;
+    double *ent = D.ent + (int64_t)S.rank * kDotEnt;
+    if (m > 0) {
+        LdExt<LD> le{ld, S.R1, D.pre + P.ext_off};
+        k_dotd_nodes<<<nblocks(8 * m), kThreads, 0, st>>>(le, n, P.cut, P.na, P.nb, D.nodes, sc, skip);
+        k_dotd_canon<<<1, 1024, 0, st>>>(D.nodes, P.na, P.nb, ent, sc, skip);
+        *launches += 2;
+    } else {
+        FLIP_CUDA_OK(cudaMemsetAsync(ent, 0, sizeof(double) * kDotEnt, st));
+    }
+    // (4) everyone's blocks, merged in index order
+    std::vector<int64_t> off(S.world + 1);
+    for (int q = 0; q <= S.world; q++) off[q] = (int64_t)q * kDotEnt * 8;
+    if (int rc = slab_allgatherv(c, D.ent, off.data())) return rc;
+    k_dotd_merge<<<1, 1, 0, st>>>(D.ent, S.world, epi, out_dev, sc, skip);
+    (*launches)++;
+    return 0;
+}
+
 // ================================================================ solvers
 struct SysView {
     int64_t n;
@@ -577,6 +824,9 @@ struct SysView {
     const unsigned short *meta = nullptr;
     const unsigned *dy = nullptr;
     const int2 *dz = nullptr;
+    // rows [r0, r0 + n) are computed (global row numbering); a slab rank's
+    // own rows, 0 otherwise
+    int64_t r0 = 0;
 };
 
 __device__ __forceinline__ double nbr_sum(const int *__restrict__ nbr, int64_t ldn, int64_t r,
@@ -597,7 +847,7 @@ __global__ void k_matvec(SysView S, const double *__restrict__ x, double *__rest
                          double *__restrict__ copy_to, const DevScalars *sc, int check_done) {
     if (check_done && sc->done) return;
     double m = 0.0;
-    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+    for (int64_t r = S.r0 + gtid(); r < S.r0 + S.n; r += gstride()) {
         double s = nbr_sum(S.nbr, S.ldn, r, x);
         double xr = x[r];
         double yr = S.scale * (S.diag[r] * xr - s);
@@ -616,7 +866,7 @@ __global__ void k_matvec(SysView S, const double *__restrict__ x, double *__rest
 // y-neighbour lies at most nx rows away.  Exact: diag holds a small integer.
 __global__ void k_compact_nbr(SysView S, unsigned short *__restrict__ meta,
                               unsigned *__restrict__ dy, int2 *__restrict__ dz) {
-    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+    for (int64_t r = S.r0 + gtid(); r < S.r0 + S.n; r += gstride()) {
         unsigned m = (unsigned)S.diag[r] << 8;
         int nb[6];
 #pragma unroll
@@ -638,7 +888,7 @@ __global__ void __launch_bounds__(256)
 k_matvec_c(SysView S, const double *__restrict__ x, double *__restrict__ y, const DevScalars *sc) {
     pdl_wait();
     if (sc->done) return;
-    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+    for (int64_t r = S.r0 + gtid(); r < S.r0 + S.n; r += gstride()) {
         const unsigned m = S.meta[r];
         const unsigned d = S.dy[r];
         const int2 z = S.dz[r];
@@ -686,7 +936,7 @@ struct LdLaneDot {
 __global__ void k_jacobi(SysView S, const double *__restrict__ x, double *__restrict__ out,
                          const DevScalars *sc, int check_done) {
     if (check_done && sc->done) return;
-    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+    for (int64_t r = S.r0 + gtid(); r < S.r0 + S.n; r += gstride()) {
         double s = nbr_sum(S.nbr, S.ldn, r, x);
         out[r] = (S.rhs[r] / S.scale + s) / S.diag[r];
     }
@@ -699,7 +949,7 @@ __global__ void k_gs_rows(SysView S, const int *__restrict__ rows, int64_t m, in
     if (check_done && sc->done) return;
     int64_t cnt = rows ? m : S.n;
     for (int64_t t = gtid(); t < cnt; t += gstride()) {
-        int64_t r = t;
+        int64_t r = rows ? t : S.r0 + t;
         if (rows) {
             r = rows[t];
         } else {
@@ -926,12 +1176,14 @@ __global__ void k_solve_init(DevScalars *sc, double tol, int64_t n, int relax) {
 }
 
 __global__ void k_check_diag(SysView S, DevScalars *sc, unsigned long long *first_bad) {
-    for (int64_t r = gtid(); r < S.n; r += gstride())
+    for (int64_t r = S.r0 + gtid(); r < S.r0 + S.n; r += gstride())
         if (!(S.diag[r] > 0.0)) atomicMin(first_bad, (unsigned long long)r);
 }
 
+constexpr unsigned long long kNoRow = 0x7f7f7f7f7f7f7f7fULL;  // memset 0x7f: no bad row
+
 __global__ void k_check_diag_final(SysView S, DevScalars *sc, const unsigned long long *first_bad) {
-    if (*first_bad != ~0ULL) {
+    if (*first_bad != kNoRow) {
         sc->status = FLIP_E_SINGULAR;
         sc->err_cell = S.cell ? S.cell[*first_bad] : (long long)*first_bad;
         sc->done = 1;
@@ -965,7 +1217,7 @@ __global__ void __launch_bounds__(256)
 k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
              const double *__restrict__ s, const double *__restrict__ q, DevScalars *sc,
              double *__restrict__ rL, const int *__restrict__ posL, int64_t max_iters,
-             double *history) {
+             double *history, int check) {
     pdl_wait();
     if (sc->done) return;
     __shared__ double wm[8];
@@ -1015,7 +1267,8 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
             sc->upd_ticket = 0u;
             const double res = __longlong_as_double(
                 (long long)atomicAdd(&sc->res_bits, 0ull));
-            iter_check_body(sc, max_iters, history, res);
+            // slab mode (check 0): the test runs after the MAX allreduce
+            if (check) iter_check_body(sc, max_iters, history, res);
         }
     }
 }
@@ -1069,6 +1322,10 @@ struct SolveCfg {
     const int *red, *black;
     int64_t nred, nblack;
     Dims d;
+    // slab mode (null otherwise): S covers the rank's own rows; `full` is
+    // the whole system for the replicated MIC(0) / GS / multigrid sweeps
+    SlabDot *slab = nullptr;
+    const SysView *full = nullptr;
 };
 
 struct SolveOut {
@@ -1153,17 +1410,54 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
 // caller's k_pcg_update and z.r dot (r already in Lb.rL, z left in Lb.zL).
 // (Scattering z into row order from inside the backward sweep instead was
 // measured slower: +36 us per sweep for -21 us in the dot at 256^3.)
+// Comm failure inside the solve loop (slab mode): the first one fails it.
+static thread_local int g_slab_err = 0;
+
+// r (own rows) -> every rank: the MIC(0) / multigrid preconditioners are
+// global recurrences, replicated on each rank of a slab decomposition.
+static void slab_gather_rows(const SolveCfg &cfg, double *v) {
+    Ctx &c = *cfg.slab->c;
+    std::vector<int64_t> off(c.slab.world + 1);
+    for (int q = 0; q <= c.slab.world; q++) off[q] = 8 * c.slab.rstart[q];
+    if (int rc = slab_allgatherv(c, v, off.data()))
+        if (!g_slab_err) g_slab_err = rc;
+}
+
+static void slab_halo(const SolveCfg &cfg, double *v) {
+    if (int rc = slab_row_halo(*cfg.slab->c, v))
+        if (!g_slab_err) g_slab_err = rc;
+}
+
+static void slab_max(const SolveCfg &cfg, unsigned long long *bits) {
+    if (int rc = slab_allreduce(*cfg.slab->c, (int64_t *)bits, 1, FLIP_OP_MAX))
+        if (!g_slab_err) g_slab_err = rc;
+}
+
+template <class LD>
+static void solver_dot(const SolveCfg &cfg, const LD &ld, int64_t n_full, double *tmp, int epi,
+                       DevScalars *sc, cudaStream_t st, int64_t *launches) {
+    if (cfg.slab) {
+        if (int rc = launch_dot_slab(*cfg.slab, ld, n_full, nullptr, epi, sc, st, launches))
+            if (!g_slab_err) g_slab_err = rc;
+        return;
+    }
+    launch_dot_f(ld, n_full, tmp, nullptr, epi, sc, st, launches);
+}
+
 static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                      const SweepLevels &LV, const double *r, double *z, DevScalars *sc,
                      cudaStream_t st, int64_t *launches, bool fused = false) {
+    const bool replicated = cfg.precond == FLIP_PRECOND_MG || cfg.precond == FLIP_PRECOND_MIC0;
+    const SysView &F = (cfg.slab && replicated) ? *cfg.full : S;  // rows the sweep covers
+    if (cfg.slab && replicated) slab_gather_rows(cfg, const_cast<double *>(r));
     if (cfg.precond == FLIP_PRECOND_MG) {
-        mg_apply(*LV.mg, r, z, S.n, sc, st, launches);
+        mg_apply(*LV.mg, r, z, F.n, sc, st, launches);
         return;
     }
     if (cfg.precond == FLIP_PRECOND_MIC0 && LV.lane) {
         // r -> L layout, forward (L), backward (L), back to rows
         const LaneBufs &Lb = *LV.lane;
-        if (!fused) launch_rows_to_lane(r, Lb.posL, S.n, Lb.rL, sc, st);
+        if (!fused || cfg.slab) launch_rows_to_lane(r, Lb.posL, F.n, Lb.rL, sc, st);
         Probe *pb = LV.probe;
         for (int rev = 0; rev < 2; rev++) {
             LaneArgs A = Lb.args;
@@ -1182,18 +1476,19 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 cudaEventRecord(pb->ev[2 * pb->used + 1], st);
                 pb->used++;
                 pb->launches++;
-                pb->bytes += 24.0 * (double)S.n;  // src + precon read, dst written per row
+                pb->bytes += 24.0 * (double)F.n;  // src + precon read, dst written per row
             }
         }
-        if (!fused) launch_lane_to_rows(Lb.zL, Lb.posL, S.n, z, sc, st);
-        *launches += 2 * 2 + (fused ? 0 : 2);
+        if (!fused) launch_lane_to_rows(Lb.zL, Lb.posL, F.n, z, sc, st);
+        *launches += 2 * 2 + (fused ? 0 : 2) + (cfg.slab && fused ? 1 : 0);
     } else if (cfg.precond == FLIP_PRECOND_MIC0) {
         // forward substitution into tq, then backward into z
-        do_sweep<SW_MIC_FWD>(S, LV, r, B.tq, B.precon, sc, st, launches);
-        do_sweep<SW_MIC_BWD>(S, LV, B.tq, z, B.precon, sc, st, launches);
+        do_sweep<SW_MIC_FWD>(F, LV, r, B.tq, B.precon, sc, st, launches);
+        do_sweep<SW_MIC_BWD>(F, LV, B.tq, z, B.precon, sc, st, launches);
     } else {
+        const int64_t o = S.r0;  // own rows (slab) or all rows
         k_precond_diag<<<nblocks(S.n), kThreads, 0, st>>>(
-            S.n, r, cfg.precond == FLIP_PRECOND_JACOBI ? B.precon : nullptr, z, sc, 1);
+            S.n, r + o, cfg.precond == FLIP_PRECOND_JACOBI ? B.precon + o : nullptr, z + o, sc, 1);
         (*launches)++;
     }
 }
@@ -1201,41 +1496,65 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
 // Runs SOLVERS[solver](sys, max_iters, tol) (pressure.py:200-332) on the
 // device.  sc->rhsmax_bits must hold max|rhs|.  Host syncs once per
 // check_every iterations to poll the done flag.
+//
+// Slab mode (cfg.slab): S covers the rank's own rows [S.r0, S.r0 + S.n) of
+// the global row vectors; before every stencil pass the rows of the
+// neighbouring planes are refreshed (slab_row_halo), max-norms are MAX-
+// allreduced, the dots run the distributed numpy tree, and the MIC(0) / GS /
+// multigrid sweeps run replicated on the gathered vector.  Every rank makes
+// the same sequence of exchanges, and every decision (done, converged) is
+// taken on globally reduced values, so all ranks stop together.
 static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                      const SweepLevels &LV, DevScalars *sc, DevScalars *sch, cudaStream_t st,
                      int64_t *launches, SolveOut *out) {
-    int64_t n = S.n;
+    const bool sl = cfg.slab != nullptr;
+    const int64_t n = S.n;                       // rows computed here
+    const int64_t o = S.r0;                      // first of them (global numbering)
+    const int64_t nf = sl ? cfg.full->n : n;     // rows of the whole system
+    Slab *SL = sl ? &cfg.slab->c->slab : nullptr;
+    g_slab_err = 0;
     bool relax = cfg.solver != FLIP_SOLVER_PCG;
-    k_solve_init<<<1, 1, 0, st>>>(sc, cfg.tol, n, relax ? 1 : 0);
-    cudaMemsetAsync(B.u64_scratch, 0xff, sizeof(unsigned long long), st);
+    k_solve_init<<<1, 1, 0, st>>>(sc, cfg.tol, nf, relax ? 1 : 0);
+    cudaMemsetAsync(B.u64_scratch, 0x7f, sizeof(unsigned long long), st);
     (*launches)++;
-    if (n > 0) {
+    if (nf > 0) {
         k_check_diag<<<nblocks(n), kThreads, 0, st>>>(S, sc, B.u64_scratch);
+        if (sl)
+            if (int rc = slab_allreduce(*cfg.slab->c, (int64_t *)B.u64_scratch, 1, FLIP_OP_MIN))
+                return rc;
         k_check_diag_final<<<1, 1, 0, st>>>(S, sc, B.u64_scratch);
         *launches += 2;
-        k_fill<<<nblocks(n), kThreads, 0, st>>>(B.x, n, 0.0);
+        k_fill<<<nblocks(nf), kThreads, 0, st>>>(B.x, nf, 0.0);
         (*launches)++;
     }
     int every = cfg.check_every > 0 ? cfg.check_every : (relax ? 64 : 8);
-    if (n > 0 && !relax) {
+    const bool lane = cfg.precond == FLIP_PRECOND_MIC0 && LV.lane;
+    if (nf > 0 && !relax) {
         if (cfg.precond == FLIP_PRECOND_MIC0) {
-            do_sweep<SW_MIC_BUILD>(S, LV, nullptr, B.precon, nullptr, sc, st, launches);
+            do_sweep<SW_MIC_BUILD>(sl ? *cfg.full : S, LV, nullptr, B.precon, nullptr, sc, st,
+                                   launches);
             if (LV.lane) {
-                launch_rows_to_lane(B.precon, LV.lane->posL, n, LV.lane->preL, sc, st);
+                launch_rows_to_lane(B.precon, LV.lane->posL, nf, LV.lane->preL, sc, st);
                 (*launches)++;
             }
         }
         else if (cfg.precond == FLIP_PRECOND_JACOBI) {
-            k_inv_diag<<<nblocks(n), kThreads, 0, st>>>(n, S.diag, S.scale, B.precon);
+            k_inv_diag<<<nblocks(n), kThreads, 0, st>>>(n, S.diag + o, S.scale, B.precon + o);
             (*launches)++;
         }
-        cudaMemcpyAsync(B.r, S.rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(B.r + o, S.rhs + o, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
         apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches);
-        cudaMemcpyAsync(B.s, B.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
-        launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA0, sc, st, launches);
+        cudaMemcpyAsync(B.s + o, B.z + o, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+        if (sl) slab_halo(cfg, B.s);
+        solver_dot(cfg, LdProd{B.z, B.r}, nf, B.dot_tmp, EPI_SIGMA0, sc, st, launches);
+    }
+    if (nf > 0 && relax && cfg.solver == FLIP_SOLVER_GS && sl) {
+        // lexicographic GS is one global recurrence: replicated on the
+        // gathered rhs (every rank then holds the same full iterate)
+        slab_gather_rows(cfg, const_cast<double *>(S.rhs));
     }
     int64_t it = 0;
-    while (n > 0 && it < cfg.max_iters) {
+    while (nf > 0 && it < cfg.max_iters) {
         int64_t batch = std::min<int64_t>(every, cfg.max_iters - it);
         for (int64_t b = 0; b < batch; b++) {
             if (!relax) {  // pressure.py:314-331
@@ -1243,9 +1562,8 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 // z.r dot (pressure.py:314-331); q = A s can be fused into the
                 // s.q dot too (FLIPB200_FUSE_MATVEC, slower: 8-lane groups
                 // coalesce the stencil gathers worse than k_matvec)
-                const bool lane = cfg.precond == FLIP_PRECOND_MIC0 && LV.lane;
                 static const bool fuse_mv = getenv("FLIPB200_FUSE_MATVEC") != nullptr;
-                if (fuse_mv) {
+                if (fuse_mv && !sl) {
                     launch_dot_f(LdMatvecDot{S, B.s, B.q}, n, B.dot_tmp, nullptr, EPI_CURV, sc,
                                  st, launches);
                 } else {
@@ -1254,46 +1572,69 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                     else
                         k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
                                                                   nullptr, sc, 1);
-                    launch_dot(B.s, B.q, n, B.dot_tmp, nullptr, EPI_CURV, sc, st, launches);
+                    solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
                     (*launches)++;
                 }
-                launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n, B.x, B.r, B.s, B.q, sc,
-                           lane ? LV.lane->rL : nullptr, lane ? LV.lane->posL : nullptr,
-                           (int64_t)cfg.max_iters, cfg.history);
+                launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n, B.x + o,
+                           B.r + o, (const double *)(B.s + o), (const double *)(B.q + o), sc,
+                           (lane && !sl) ? LV.lane->rL : nullptr,
+                           (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
+                           (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1);
+                if (sl) {
+                    slab_max(cfg, &sc->res_bits);
+                    k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
+                    (*launches)++;
+                }
                 apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
                 if (lane)
-                    launch_dot_f(LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, n, B.dot_tmp,
-                                 nullptr, EPI_SIGMA_NEW, sc, st, launches);
+                    solver_dot(cfg, LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, nf, B.dot_tmp,
+                               EPI_SIGMA_NEW, sc, st, launches);
                 else
-                    launch_dot(B.z, B.r, n, B.dot_tmp, nullptr, EPI_SIGMA_NEW, sc, st, launches);
-                launch_pdl(k_pcg_dir, wave_blocks(k_pcg_dir, n), kThreads, 0, st, n, B.s, B.z, sc);
+                    solver_dot(cfg, LdProd{B.z, B.r}, nf, B.dot_tmp, EPI_SIGMA_NEW, sc, st,
+                               launches);
+                launch_pdl(k_pcg_dir, wave_blocks(k_pcg_dir, n), kThreads, 0, st, n, B.s + o,
+                           (const double *)(B.z + o), (const DevScalars *)sc);
+                if (sl) slab_halo(cfg, B.s);
                 *launches += 2;  // update (with the convergence test) + dir
             } else {  // pressure.py:209-213
                 if (cfg.solver == FLIP_SOLVER_JACOBI) {
                     k_jacobi<<<nblocks(n), kThreads, 0, st>>>(S, B.x, B.xtmp, sc, 1);
+                    if (sl) slab_halo(cfg, B.xtmp);
                     k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.xtmp, nullptr, S.rhs, &sc->res_bits,
                                                               B.x, sc, 1);
+                    if (sl) {  // the halo rows of x follow xtmp's
+                        cudaMemcpyAsync(B.x + SL->Rlo, B.xtmp + SL->Rlo,
+                                        sizeof(double) * (SL->R0 - SL->Rlo), cudaMemcpyDeviceToDevice, st);
+                        cudaMemcpyAsync(B.x + SL->R1, B.xtmp + SL->R1,
+                                        sizeof(double) * (SL->Rhi - SL->R1), cudaMemcpyDeviceToDevice, st);
+                    }
                     *launches += 2;
                 } else {
+                    bool gs_oop = cfg.solver == FLIP_SOLVER_GS && LV.wave;
                     if (cfg.solver == FLIP_SOLVER_GS) {
+                        const SysView &F = sl ? *cfg.full : S;
                         if (LV.wave) {  // out of place: old x in, new x out, copied back below
-                            do_sweep<SW_GS>(S, LV, B.x, B.xtmp, nullptr, sc, st, launches);
+                            do_sweep<SW_GS>(F, LV, B.x, B.xtmp, nullptr, sc, st, launches);
                         } else {
-                            do_sweep<SW_GS>(S, LV, nullptr, B.x, nullptr, sc, st, launches);
+                            do_sweep<SW_GS>(F, LV, nullptr, B.x, nullptr, sc, st, launches);
                         }
                     } else {
                         k_gs_rows<<<nblocks(cfg.red ? cfg.nred : n), kThreads, 0, st>>>(
                             S, cfg.red, cfg.nred, 0, cfg.d, B.x, sc, 1);
+                        if (sl) slab_halo(cfg, B.x);
                         k_gs_rows<<<nblocks(cfg.black ? cfg.nblack : n), kThreads, 0, st>>>(
                             S, cfg.black, cfg.nblack, 1, cfg.d, B.x, sc, 1);
+                        if (sl) slab_halo(cfg, B.x);
                         *launches += 2;
                     }
-                    bool gs_oop = cfg.solver == FLIP_SOLVER_GS && LV.wave;
                     k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, gs_oop ? B.xtmp : B.x, nullptr,
                                                               S.rhs, &sc->res_bits,
-                                                              gs_oop ? B.x : nullptr, sc, 1);
+                                                              (gs_oop && !sl) ? B.x : nullptr, sc, 1);
+                    if (gs_oop && sl)  // the replicated iterate, every row
+                        cudaMemcpyAsync(B.x, B.xtmp, sizeof(double) * nf, cudaMemcpyDeviceToDevice, st);
                     (*launches)++;
                 }
+                if (sl) slab_max(cfg, &sc->res_bits);
                 k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
                 (*launches)++;
             }
@@ -1301,8 +1642,11 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
         it += batch;
         cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
         FLIP_CUDA_OK(cudaStreamSynchronize(st));
+        if (g_slab_err) return g_slab_err;
         if (sch->done) break;
     }
+    if (sl && nf > 0 && !relax) slab_halo(cfg, B.x);  // pressure_field reads planes k0-1, k1
+    if (g_slab_err) return g_slab_err;
     cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
     FLIP_CUDA_OK(cudaStreamSynchronize(st));
     FLIP_CUDA_OK(cudaGetLastError());
@@ -1339,10 +1683,33 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     exclusive_scan(in, nc, c.rowscan, &c.sc->nrows, c.scan_tmp, st);
     k_rows_compact<<<nblocks(nc), kThreads, 0, st>>>(in, nc, c.rowscan, c.isrow, c.cell_of_row, c.sc);
     k_bbox_reset<<<1, 1, 0, st>>>(c.sc);
-    k_assemble_rows<<<nblocks(nc), kThreads, 0, st>>>(c.d, c.label, c.isrow, c.rowscan,
-                                                      c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr, nc,
-                                                      c.diagd, c.rhs, &c.sc->rhsmax_bits, c.sc);
-    c.launches += 8;
+    c.launches += 6;
+    bool need_sweeps = prm.solver == FLIP_SOLVER_GS ||
+                       (prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MIC0);
+    Slab &SL = c.slab;
+    SlabDot SD{&c};
+    if (!SL.on) {
+        k_assemble_rows<<<nblocks(nc), kThreads, 0, st>>>(c.d, c.label, c.isrow, c.rowscan,
+                                                          c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr,
+                                                          nc, c.diagd, c.rhs, &c.sc->rhsmax_bits,
+                                                          c.sc, (int64_t)0, (int64_t)-1,
+                                                          (int64_t)0, (int64_t)-1);
+        c.launches += 2;
+    } else {
+        // the rows are numbered globally (every rank labelled every plane):
+        // own rows [R0, R1) and the halo rows of planes k0-1 / k1
+        if (int rc = slab_rows(c)) return rc;
+        const bool full = need_sweeps || (prm.solver == FLIP_SOLVER_PCG &&
+                                          prm.precond == FLIP_PRECOND_MG);
+        // structure (diag, neighbours, bounding box) of every row when a
+        // replicated sweep needs it, else of the window; rhs of the own rows
+        const int64_t a_lo = full ? 0 : SL.Rlo, a_hi = full ? SL.rstart[SL.world] : SL.Rhi;
+        k_assemble_rows<<<nblocks(std::max<int64_t>(a_hi - a_lo, 1)), kThreads, 0, st>>>(
+            c.d, c.label, c.isrow, c.rowscan, c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr, nc,
+            c.diagd, c.rhs, &c.sc->rhsmax_bits, c.sc, a_lo, a_hi, SL.R0, SL.R1);
+        c.launches++;
+        if (int rc = slab_allreduce(c, (int64_t *)&c.sc->rhsmax_bits, 1, FLIP_OP_MAX)) return rc;
+    }
     cudaMemcpyAsync(c.sch, c.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
     FLIP_CUDA_OK(cudaStreamSynchronize(st));
     int64_t n = c.sch->nrows;
@@ -1352,9 +1719,14 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     // scale = dt / (rho * dtau**2) (pressure.py:164), same IEEE division as the reference
     double scale = dt / prm.rho_dtau2_h;
     SysView S{n, c.cell_of_row, c.nbr, nc, c.diagd, c.rhs, scale};
+    SysView Sfull = S;
+    if (SL.on) {  // this rank computes its own rows
+        S.r0 = SL.R0;
+        S.n = SL.R1 - SL.R0;
+    }
     static const bool plain_mv = getenv("FLIPB200_PLAIN_MATVEC") != nullptr;
     if (prm.solver == FLIP_SOLVER_PCG && n > 0 && c.d.nx < 32768 && !plain_mv) {
-        k_compact_nbr<<<nblocks(n), kThreads, 0, st>>>(S, c.nb_meta, c.nb_dy, c.nb_dz);
+        k_compact_nbr<<<nblocks(S.n), kThreads, 0, st>>>(S, c.nb_meta, c.nb_dy, c.nb_dz);
         c.launches++;
         S.meta = c.nb_meta;
         S.dy = c.nb_dy;
@@ -1363,9 +1735,7 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     // sequential sweeps (GS, MIC(0)) run as the pipelined wavefront over the
     // rows' bounding box; FLIPB200_LEVEL_SWEEPS=1 selects the level-scheduled
     // cooperative fallback (same results, used to cross-check)
-    static const bool level_sweeps = getenv("FLIPB200_LEVEL_SWEEPS") != nullptr;
-    bool need_sweeps = prm.solver == FLIP_SOLVER_GS ||
-                       (prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MIC0);
+    static const bool level_sweeps = getenv("FLIPB200_LEVEL_SWEEPS") != nullptr && !SL.on;
     Levels L{c.lvl, c.lvl_cnt, c.lvl_off, c.lvl_rows, &c.sc->nlevels, 0};
     WaveArgs W{};
     bool use_wave = need_sweeps && n > 0 && !level_sweeps;
@@ -1398,8 +1768,18 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     static const bool no_lane = getenv("FLIPB200_NO_LANE") != nullptr;
     bool use_lane = use_wave && prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MIC0 &&
                     !no_lane && lane_entries(W.geom) <= c.lane_cap;
+    // the substitutions run 2 x 2 pencils per thread (k_mic_quad) when their
+    // lane layout and halos fit the buffers sized for the 16 x 16 geometry
+    WaveGeom LG = W.geom;
+    if (use_lane && mic_quad_enabled()) {
+        WaveGeom qg = quad_geom(c.sch->row_lo, c.sch->row_hi);
+        const int64_t halo_need = (int64_t)qg.TB * qg.TC * qg.nsteps * 64;
+        if (lane_entries(qg) <= c.lane_cap &&
+            halo_need <= wave_halo_doubles(c.d.nx, c.d.ny, c.d.nz) - 64)
+            LG = qg;
+    }
     if (use_lane) {
-        LB.args.geom = W.geom;
+        LB.args.geom = LG;
         LB.args.halo_y = W.halo_y;
         LB.args.halo_z = W.halo_z;
         LB.args.scale = scale;
@@ -1412,7 +1792,7 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         LB.tqL = c.laneB;
         LB.zL = c.laneC;
         LB.preL = c.laneD;
-        launch_lane_map(W.geom, c.d, c.isrow, c.rowscan, c.lrow, c.posL, c.laneA, c.laneB, st);
+        launch_lane_map(LG, c.d, c.isrow, c.rowscan, c.lrow, c.posL, c.laneA, c.laneB, st);
         c.launches++;
     }
     SweepLevels LV{&L, &L, &L, 1, use_wave ? &W : nullptr, &c.probe, use_lane ? &LB : nullptr, &c};
@@ -1420,6 +1800,10 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         if (int rc = mg_setup(c, scale, c.sch->row_lo, c.sch->row_hi, st)) return rc;
     SolveCfg cfg{prm.solver, prm.precond, prm.max_iters, prm.tol, prm.solver_check_every, nullptr,
                  nullptr, nullptr, 0, 0, c.d};
+    if (SL.on) {
+        cfg.slab = &SD;
+        cfg.full = &Sfull;
+    }
     SolveBufs B{c.x, c.r, c.z, c.s, c.q, c.tq, c.precon, c.xtmp, c.dot_part, c.scan_tmp,
                 c.u64_scratch};
     SolveOut o{};
@@ -1438,6 +1822,15 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     rep->err_iteration = o.err_it;
     rep->err_value = o.err_value;
     if (o.status) return 0;
+    if (SL.on) {  // own planes and the two next to them (the gradient reads them)
+        const int64_t pc = (int64_t)c.d.nx * c.d.ny;
+        const int64_t c0 = std::max<int64_t>(SL.k0 - 1, 0) * pc;
+        const int64_t c1 = std::min<int64_t>(SL.k1 + 1, c.d.nz) * pc;
+        k_pressure_field<<<nblocks(c1 - c0), kThreads, 0, st>>>(c.p + c0, c1 - c0, c.isrow + c0,
+                                                               c.rowscan + c0, c.x);
+        c.launches++;
+        return 0;
+    }
     k_pressure_field<<<nblocks(nc), kThreads, 0, st>>>(c.p, nc, c.isrow, c.rowscan, c.x);
     c.launches++;
     return 0;

@@ -834,8 +834,16 @@ __global__ void k_lane_map(WaveGeom G, Dims d, int TY, int TZ, const uint8_t *__
         int s = (int)(ts - tq * (unsigned)G.nsteps);
         int tile = (int)tq;
         int b = tile / G.TC, c = tile % G.TC;
-        int jj = p % TY, kk = p / TY;
-        int i = G.ilo + s - jj - kk, j = G.jlo + b * TY + jj, k = G.klo + c * TZ + kk;
+        int i, j, k;
+        if (G.quad) {  // [q][thread]: thread (jj, kk) of 16 x 16 owns pencils (2jj + a, 2kk + b)
+            const int q = p >> 8, th = p & 255, jj = th & 15, kk = th >> 4;
+            i = G.ilo + s - jj - kk;
+            j = G.jlo + b * TY + 2 * jj + (q & 1);
+            k = G.klo + c * TZ + 2 * kk + (q >> 1);
+        } else {
+            int jj = p % TY, kk = p / TY;
+            i = G.ilo + s - jj - kk, j = G.jlo + b * TY + jj, k = G.klo + c * TZ + kk;
+        }
         int row = -1;
         if (i >= G.ilo && i <= G.ihi && j <= G.jhi && k <= G.khi) {
             int64_t cell = i + (int64_t)j * d.nx + (int64_t)k * d.nx * d.ny;
@@ -1105,6 +1113,20 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
 }
 
 cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st) {
+    if (A.geom.quad) {
+        // cross-cluster faces only (as k_wave_prep_cl for k_mic_cl), 32 wide
+        const int64_t tiles = (int64_t)A.geom.TB * A.geom.TC;
+        int cy = 0, cz = 0;
+        quad_cluster_shape(&cy, &cz);
+        const int64_t nsel = (int64_t)(A.geom.TB / cy) * A.geom.TC * A.geom.nsteps * 32 +
+                             (int64_t)A.geom.TB * (A.geom.TC / cz) * A.geom.nsteps * 32;
+        LaneArgs B = A;
+        B.halo_z = A.halo_y + tiles * A.geom.nsteps * 32;
+        launch_pdl(k_wave_prep_cl, nblocks(nsel), kThreads, 0, st, A.halo_y, B.halo_z,
+                   A.geom.TB, A.geom.TC, A.geom.nsteps, 32, 32, cy, cz, rev ? 1 : 0, A.ticket,
+                   (const DevScalars *)A.sc);
+        return launch_mic_quad(rev, B, st);
+    }
     TileShape t = wave_shape();
 #define LANE_CASE(a, b)                                                                   \
     if (t.ty == a && t.tz == b)                                                           \

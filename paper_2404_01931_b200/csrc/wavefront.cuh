@@ -33,6 +33,7 @@ struct WaveGeom {
     int nsteps;                         // x span + ty + tz - 2
     int ispan;                          // ihi - ilo + 1
     int ispan_pad;                      // ispan rounded up to even (halo lane stride)
+    int quad = 0;                       // 1: k_mic_quad geometry (2 x 2 pencils per thread)
 };
 
 struct WaveArgs {
@@ -161,6 +162,14 @@ struct LaneArgs {
 };
 
 cudaError_t launch_wave(int mode, const WaveArgs &A, cudaStream_t st);
+// wavequad.cu: 2 x 2 pencils per thread (FLIPB200_QUAD=0 disables)
+bool mic_quad_enabled();
+int quad_cluster_shape(int *cy, int *cz);
+WaveGeom quad_geom(const int lo[3], const int hi[3]);
+cudaError_t launch_mic_quad(bool rev, const LaneArgs &A, cudaStream_t st);
+__global__ void k_wave_prep_cl(double *halo_y, double *halo_z, int TB, int TC, int nsteps, int ty,
+                               int tz, int cy, int cz, int rev, int *ticket, const DevScalars *sc);
+__global__ void k_wave_prep(double *halo, int64_t nh, int *ticket, const DevScalars *sc);
 cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st);
 // wavecl.cu: cluster/DSMEM variant (FLIPB200_CLUSTER=CYxCZ); NotSupported if off
 cudaError_t launch_mic_cluster(bool rev, const LaneArgs &A, cudaStream_t st);

@@ -1,0 +1,476 @@
+// wavequad.cu — MIC(0) forward/backward substitution (_core.pyx:311-347) as
+// a tiled wavefront in which every thread owns a 2 x 2 block of x-pencils.
+//
+// k_mic_cl (wavecl.cu) gives each thread one pencil: a sweep then costs
+// about ispan + jspan + kspan dependent steps (one CTA barrier each), ~529
+// at 256^3.  Here thread (jj, kk) of a 16 x 16 tile owns pencils
+// (2jj + a, 2kk + b), a, b in {0, 1}, and at step s visits i = ilo + s - jj
+// - kk in all four.  Inside a step the four cells are evaluated in their
+// dependency order (forward: (0,0); then (1,0) and (0,1); then (1,1) --
+// each reads its in-thread -y / -z neighbour from the same step), so the
+// dependent-step count drops to about ispan + jspan/2 + kspan/2 (~307 at
+// 256^3) for a longer chain per step.  Tiles (32 x 32 pencils) exchange
+// faces two values wide through DSMEM inside a cluster and through the
+// step-major global halo across clusters, as in k_mic_cl.
+//
+// Arithmetic and operation order per cell are k_mic_cl's (absent
+// neighbours are -0.0, an exact no-op), so results are bit-identical.
+// Lane layout (k_lane_map with quad geometry): L[tile][step][q][thread],
+// q = a + 2b, i.e. 1024 entries per tile-step, one coalesced 8-byte load
+// per thread per q.
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
+#include "ops.cuh"
+#include "wavefront.cuh"
+
+namespace flip {
+
+namespace {
+
+constexpr int QT = 16;          // threads per tile edge
+constexpr int QP = QT * QT;     // compute threads
+constexpr int QW = 2 * QT;      // face width (values per step)
+
+__device__ __forceinline__ unsigned q_smem(const void *p) { return smem_u32(p); }
+__device__ __forceinline__ unsigned q_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned q_map(const void *p, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(q_smem(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void q_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ void q_st_remote(unsigned addr, double v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(addr),
+                 "l"(__double_as_longlong(v))
+                 : "memory");
+}
+__device__ __forceinline__ int q_ld_remote_int(unsigned addr) {
+    int v;
+    asm volatile("ld.relaxed.cluster.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ double q_poll(const double *p) {
+    unsigned long long v;
+    const unsigned a = q_smem(p);
+    do {
+        asm volatile("ld.relaxed.cluster.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    } while (v == WAVE_PENDING);
+    return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ double q_peek(const double *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.cluster.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(q_smem(p)) : "memory");
+    return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ double q_take(double pre, const double *p) {
+    return is_pending(pre) ? q_poll(p) : pre;
+}
+__device__ __forceinline__ double q_spin_gpu(const double *p) {
+    unsigned long long v;
+    do {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    } while (v == WAVE_PENDING);
+    return __longlong_as_double((long long)v);
+}
+
+__device__ __forceinline__ void q_cluster_tile(int t, int CB, int CC, int &bq, int &cq) {
+    int d = 0;
+    while (true) {
+        int blo = max(0, d - (CC - 1)), bhi = min(CB - 1, d);
+        int cnt = bhi - blo + 1;
+        if (t < cnt) {
+            bq = blo + t;
+            cq = d - bq;
+            return;
+        }
+        t -= cnt;
+        d++;
+    }
+}
+
+}  // namespace
+
+// One cell of the substitution (k_mic_cl's arithmetic).  pv / yv / zv are
+// the contributions of the -x / -y / -z (forward) or +x / +y / +z
+// (backward) neighbours; returns the value passed on, -0.0 off the rows.
+template <bool REV>
+__device__ __forceinline__ double mic_cell(double a, double pr, double pv, double yv, double zv,
+                                           double sc, bool row, double *dst) {
+    double o;
+    if (!REV) {  // _core.pyx:322-332
+        double tt = ((a + pv) + yv) + zv;
+        double q = tt * pr;
+        if (row) *dst = q;
+        o = (sc * pr) * q;
+    } else {     // _core.pyx:333-346
+        double sp = sc * pr;
+        double tt = ((a + sp * pv) + sp * yv) + sp * zv;
+        o = tt * pr;
+        if (row) *dst = o;
+    }
+    return row ? o : -0.0;
+}
+
+template <bool REV, int CY, int CZ, int KC, int NB>
+__global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
+    constexpr int DY = QT - 1, DZ = QT - 1;
+    // logical cell L (forward order (0,0), (1,0), (0,1), (1,1)) -> stored q
+    // (pencil a + 2b); the backward sweep visits the block mirrored
+    auto PQ = [](int L) { return REV ? 3 - L : L; };
+    // sq[buf][kk + 1][jj + 1][q]: each thread's four outputs of a step
+    __shared__ double sq[2][QT + 2][QT + 2][4];
+    __shared__ int s_tile;
+    __shared__ __align__(8) unsigned long long mbar[NB];
+    // yring[nsteps][QW], zring[nsteps][QW], then the operand chunks
+    extern __shared__ __align__(128) double ring[];
+    const int t = threadIdx.x;
+    pdl_wait();
+    if (A.sc && A.sc->done) return;
+    const WaveGeom G = A.geom;
+    const int nsteps = G.nsteps;
+    double *yring = ring, *zring = ring + (int64_t)nsteps * QW;
+    const unsigned cr = q_rank();
+    const int ry = (int)cr / CZ, rz = (int)cr % CZ;
+    const double nz0 = -0.0;
+    const double pend = __longlong_as_double((long long)WAVE_PENDING);
+    for (int q = t; q < 2 * (QT + 2) * (QT + 2) * 4; q += blockDim.x) (&sq[0][0][0][0])[q] = nz0;
+    for (int q = t; q < nsteps * 2 * QW; q += blockDim.x) ring[q] = pend;
+    if (cr == 0 && t == 0) s_tile = atomicAdd(A.ticket, 1);
+    if (t == 0) {
+        for (int q = 0; q < NB; q++) mbar_init(&mbar[q], 1);
+        mbar_fence_init();
+    }
+    q_cluster_sync();
+    const int tk = cr == 0 ? s_tile : q_ld_remote_int(q_map(&s_tile, 0));
+    int bq, cq;
+    q_cluster_tile(tk, G.TB / CY, G.TC / CZ, bq, cq);
+    int b = bq * CY + ry, c = cq * CZ + rz;
+    if (REV) {
+        b = G.TB - 1 - b;
+        c = G.TC - 1 - c;
+    }
+    const int tile = b * G.TC + c;
+    auto lstep = [&](int s) { return REV ? nsteps - 1 - s : s; };
+    const bool ydin = ry > 0, ydout = ry < CY - 1;
+    const bool zdin = rz > 0, zdout = rz < CZ - 1;
+    constexpr int TS = 4 * QP;  // lane entries per tile-step
+    double *opb = ring + (int64_t)nsteps * 2 * QW;
+    const int nch = (nsteps + KC - 1) / KC;
+    auto issue = [&](int ch) {
+        if (ch >= nch) return;
+        const int64_t tbase = (int64_t)tile * nsteps * TS;
+        const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
+        const int lo = REV ? nsteps - s0 - cnt : s0;
+        const int buf = ch % NB;
+        const unsigned bytes = (unsigned)(cnt * TS * 8);
+        mbar_expect_tx(&mbar[buf], 2 * bytes);
+        bulk_g2s(opb + (buf * 2 + 0) * KC * TS, A.src + tbase + (int64_t)lo * TS, bytes, &mbar[buf]);
+        bulk_g2s(opb + (buf * 2 + 1) * KC * TS, A.precon + tbase + (int64_t)lo * TS, bytes,
+                 &mbar[buf]);
+    };
+    // neighbour-thread offsets in sq: forward reads jj-1 / kk-1, backward jj+1 / kk+1
+    const int nbo = REV ? 2 : 0;
+
+    if (t >= QP) {
+        // ------------------- helper warp: faces across cluster boundaries
+        // lane l carries y-face word l (consumer kk = l/2; e = 0 feeds
+        // logical cell 0, e = 1 cell 2) and z-face word l (consumer jj =
+        // l/2; e = 0 feeds cell 0, e = 1 cell 1)
+        const int l = t - QP;
+        const double *iny = nullptr, *inz = nullptr;
+        {
+            const bool has = REV ? b + 1 < G.TB : b > 0;
+            if (has && !ydin)
+                iny = A.halo_y + (int64_t)(REV ? tile + G.TC : tile - G.TC) * nsteps * QW + l;
+            const bool hasz = REV ? c + 1 < G.TC : c > 0;
+            if (hasz && !zdin)
+                inz = A.halo_z + (int64_t)(REV ? tile + 1 : tile - 1) * nsteps * QW + l;
+        }
+        // where the value lands: the consumer reads its -y (-z) neighbour
+        // thread's stored output of the producing logical cell
+        const int e = l & 1, h = l >> 1;
+        const int y_row = h + 1, y_col = REV ? QT + 1 : 0, y_q = PQ(e == 0 ? 1 : 3);
+        const int z_row = REV ? QT + 1 : 0, z_col = h + 1, z_q = PQ(e == 0 ? 2 : 3);
+        // the consumer lanes must lie in the rows' box
+        const int cons_j = REV ? QT - 1 : 0, cons_k = REV ? QT - 1 : 0;
+        if (!(G.jlo + b * QW + 2 * cons_j <= G.jhi && G.klo + c * QW + 2 * h <= G.khi)) iny = nullptr;
+        if (!(G.jlo + b * QW + 2 * h <= G.jhi && G.klo + c * QW + 2 * cons_k <= G.khi)) inz = nullptr;
+        if (l == 0)
+            for (int q = 0; q < NB; q++) issue(q);
+        double hy = nz0, hz = nz0;
+        if (iny) hy = DY < nsteps ? q_spin_gpu(iny + (int64_t)DY * QW) : nz0;
+        if (inz) hz = DZ < nsteps ? q_spin_gpu(inz + (int64_t)DZ * QW) : nz0;
+        if (iny) sq[1][y_row][y_col][y_q] = hy;
+        if (inz) sq[1][z_row][z_col][z_q] = hz;
+        double py = (iny && 1 + DY < nsteps) ? ld_relaxed(iny + (int64_t)(1 + DY) * QW) : nz0;
+        double pz = (inz && 1 + DZ < nsteps) ? ld_relaxed(inz + (int64_t)(1 + DZ) * QW) : nz0;
+        for (int s = 0; s < nsteps; s++) {
+            __syncthreads();
+            if (l == 0 && s > 0 && s % KC == 0) {
+                fence_proxy_async();
+                issue(s / KC - 1 + NB);
+            }
+            const int cur = s & 1;
+            if (iny) {
+                double v = (s + 1 + DY < nsteps) ? py : nz0;
+                if (is_pending(v)) v = q_spin_gpu(iny + (int64_t)(s + 1 + DY) * QW);
+                sq[cur][y_row][y_col][y_q] = v;
+                py = (s + 2 + DY < nsteps) ? ld_relaxed(iny + (int64_t)(s + 2 + DY) * QW) : nz0;
+            }
+            if (inz) {
+                double v = (s + 1 + DZ < nsteps) ? pz : nz0;
+                if (is_pending(v)) v = q_spin_gpu(inz + (int64_t)(s + 1 + DZ) * QW);
+                sq[cur][z_row][z_col][z_q] = v;
+                pz = (s + 2 + DZ < nsteps) ? ld_relaxed(inz + (int64_t)(s + 2 + DZ) * QW) : nz0;
+            }
+        }
+        __syncthreads();
+    } else {
+        // ----------------------------------------------------- compute warps
+        const int jj = t % QT, kk = t / QT;
+        const int jbase = G.jlo + b * QW + 2 * jj, kbase = G.klo + c * QW + 2 * kk;
+        // logical cell -> in the rows' box (pencil offsets mirrored backward)
+        bool valid[4];
+#pragma unroll
+        for (int L = 0; L < 4; L++) {
+            const int q = PQ(L);
+            valid[L] = jbase + (q & 1) <= G.jhi && kbase + (q >> 1) <= G.khi;
+        }
+        const int cons_j = REV ? QT - 1 : 0, cons_k = REV ? QT - 1 : 0;
+        const int prod_j = REV ? 0 : QT - 1, prod_k = REV ? 0 : QT - 1;
+        const bool yin = ydin && jj == cons_j;
+        const bool zin = zdin && kk == cons_k;
+        // producing lanes: DSMEM into the next CTA of the cluster, or the
+        // global halo when the face leaves the cluster
+        const unsigned yout = (ydout && jj == prod_j) ? q_map(yring + 2 * kk, cr + CZ) : 0u;
+        const unsigned zout = (zdout && kk == prod_k) ? q_map(zring + 2 * jj, cr + 1) : 0u;
+        double *gy = (!ydout && jj == prod_j) ? A.halo_y + (int64_t)tile * nsteps * QW + 2 * kk : nullptr;
+        double *gz = (!zdout && kk == prod_k) ? A.halo_z + (int64_t)tile * nsteps * QW + 2 * jj : nullptr;
+        const int64_t base = (int64_t)tile * nsteps * TS + t;
+        double *dstL = A.dst + base;
+        double pv[4] = {nz0, nz0, nz0, nz0};
+        double ypre0 = pend, ypre1 = pend, zpre0 = pend, zpre1 = pend;
+        if (yin && DY < nsteps) {
+            ypre0 = q_peek(yring + DY * QW + 2 * kk);
+            ypre1 = q_peek(yring + DY * QW + 2 * kk + 1);
+        }
+        if (zin && DZ < nsteps) {
+            zpre0 = q_peek(zring + DZ * QW + 2 * jj);
+            zpre1 = q_peek(zring + DZ * QW + 2 * jj + 1);
+        }
+        const double sc = A.scale;
+        const int yr = kk + 1, yc = jj + nbo, zr = kk + nbo, zc = jj + 1;
+        for (int ch = 0; ch < nch; ch++) {
+            const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
+            const int buf = ch % NB;
+            mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
+            const double *ab = opb + (buf * 2 + 0) * KC * TS + t;
+            const double *pb = opb + (buf * 2 + 1) * KC * TS + t;
+#pragma unroll
+            for (int u = 0; u < KC; u++) {
+                if (u >= cnt) break;
+                const int s = s0 + u;
+                __syncthreads();
+                const int cur = s & 1, prv = cur ^ 1;
+                const int idx = REV ? cnt - 1 - u : u;
+                double a[4], pr[4];
+#pragma unroll
+                for (int L = 0; L < 4; L++) {
+                    a[L] = ab[idx * TS + PQ(L) * QP];
+                    pr[L] = pb[idx * TS + PQ(L) * QP];
+                }
+                // neighbour contributions from the previous step: -y feeds
+                // logical cells 0 and 2 (the -y thread's cells 1 and 3), -z
+                // feeds cells 0 and 1 (the -z thread's cells 2 and 3)
+                double y0 = sq[prv][yr][yc][PQ(1)], y2 = sq[prv][yr][yc][PQ(3)];
+                double z0 = sq[prv][zr][zc][PQ(2)], z1 = sq[prv][zr][zc][PQ(3)];
+                if (yin) {
+                    if (s + DY < nsteps) {
+                        y0 = q_take(ypre0, yring + (s + DY) * QW + 2 * kk);
+                        y2 = q_take(ypre1, yring + (s + DY) * QW + 2 * kk + 1);
+                    } else {
+                        y0 = y2 = nz0;
+                    }
+                    if (s + 1 + DY < nsteps) {
+                        ypre0 = q_peek(yring + (s + 1 + DY) * QW + 2 * kk);
+                        ypre1 = q_peek(yring + (s + 1 + DY) * QW + 2 * kk + 1);
+                    }
+                }
+                if (zin) {
+                    if (s + DZ < nsteps) {
+                        z0 = q_take(zpre0, zring + (s + DZ) * QW + 2 * jj);
+                        z1 = q_take(zpre1, zring + (s + DZ) * QW + 2 * jj + 1);
+                    } else {
+                        z0 = z1 = nz0;
+                    }
+                    if (s + 1 + DZ < nsteps) {
+                        zpre0 = q_peek(zring + (s + 1 + DZ) * QW + 2 * jj);
+                        zpre1 = q_peek(zring + (s + 1 + DZ) * QW + 2 * jj + 1);
+                    }
+                }
+                double *d = dstL + (int64_t)lstep(s) * TS;
+                double o[4];
+                o[0] = mic_cell<REV>(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), d + PQ(0) * QP);
+                o[1] = mic_cell<REV>(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), d + PQ(1) * QP);
+                o[2] = mic_cell<REV>(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), d + PQ(2) * QP);
+                o[3] = mic_cell<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), d + PQ(3) * QP);
+#pragma unroll
+                for (int L = 0; L < 4; L++) {
+                    sq[cur][kk + 1][jj + 1][PQ(L)] = o[L];
+                    pv[L] = o[L];
+                }
+                if (yout) {
+                    q_st_remote(yout + (unsigned)(s * QW * 8), o[1]);
+                    q_st_remote(yout + (unsigned)(s * QW * 8 + 8), o[3]);
+                }
+                if (zout) {
+                    q_st_remote(zout + (unsigned)(s * QW * 8), o[2]);
+                    q_st_remote(zout + (unsigned)(s * QW * 8 + 8), o[3]);
+                }
+                if (gy) {
+                    publish(gy + (int64_t)s * QW, o[1]);
+                    publish(gy + (int64_t)s * QW + 1, o[3]);
+                }
+                if (gz) {
+                    publish(gz + (int64_t)s * QW, o[2]);
+                    publish(gz + (int64_t)s * QW + 1, o[3]);
+                }
+            }
+        }
+        __syncthreads();  // matches the helper's final barrier
+    }
+    q_cluster_sync();  // no CTA leaves while a peer can still store into its rings
+}
+
+// ------------------------------------------------------------- launching --
+int quad_cluster_shape(int *cy, int *cz) {
+    static int y = -1, z = -1;
+    if (y < 0) {
+        y = 2;
+        z = 4;
+        if (const char *e = getenv("FLIPB200_QUAD_CLUSTER")) {
+            int a = 0, b = 0;
+            if (sscanf(e, "%dx%d", &a, &b) == 2) {
+                y = a;
+                z = b;
+            }
+        }
+    }
+    *cy = y;
+    *cz = z;
+    return 1;
+}
+
+bool mic_quad_enabled() {
+    static const int on = [] {
+        const char *e = getenv("FLIPB200_QUAD");
+        return e ? atoi(e) : 1;
+    }();
+    return on != 0;
+}
+
+// Quad geometry: tiles of 32 x 32 pencils, 16 x 16 threads, padded to whole
+// clusters; nsteps = ispan + 2 * (16 - 1).
+WaveGeom quad_geom(const int lo[3], const int hi[3]) {
+    int cy, cz;
+    quad_cluster_shape(&cy, &cz);
+    WaveGeom g{};
+    g.ilo = lo[0];
+    g.ihi = hi[0];
+    g.jlo = lo[1];
+    g.jhi = hi[1];
+    g.klo = lo[2];
+    g.khi = hi[2];
+    g.ty = QW;
+    g.tz = QW;
+    g.TB = (hi[1] - lo[1] + QW) / QW;
+    g.TC = (hi[2] - lo[2] + QW) / QW;
+    g.TB = (g.TB + cy - 1) / cy * cy;
+    g.TC = (g.TC + cz - 1) / cz * cz;
+    g.ispan = hi[0] - lo[0] + 1;
+    g.ispan_pad = (g.ispan + 1) & ~1;
+    g.nsteps = g.ispan + 2 * (QT - 1);
+    g.quad = 1;
+    return g;
+}
+
+template <bool REV, int CY, int CZ, int KC, int NB>
+static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
+    const int tiles = A.geom.TB * A.geom.TC;
+    const size_t rings = ((size_t)A.geom.nsteps * 2 * QW * sizeof(double) + 127) / 128 * 128;
+    const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double);
+    static cudaError_t attr = [] {
+        cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, CY, CZ, KC, NB>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024 - 24 * 1024);
+        if (e == cudaSuccess && CY * CZ > 8)
+            e = cudaFuncSetAttribute(k_mic_quad<REV, CY, CZ, KC, NB>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return e;
+    }();
+    if (attr != cudaSuccess) return attr;
+    if (smem > 227 * 1024 - 24 * 1024) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tiles);
+    cfg.blockDim = dim3(QP + 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CY * CZ;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_quad<REV, CY, CZ, KC, NB>, A);
+    return e != cudaSuccess ? e : cudaPeekAtLastError();
+}
+
+static int quad_chunks() {
+    static int v = -1;
+    if (v < 0) {
+        int a = 2, b = 3;
+        if (const char *e = getenv("FLIPB200_QUAD_CHUNKS")) sscanf(e, "%dx%d", &a, &b);
+        v = a * 100 + b;
+    }
+    return v;
+}
+
+template <bool REV, int CY, int CZ>
+static cudaError_t launch_quad_c(const LaneArgs &A, cudaStream_t st) {
+    switch (quad_chunks()) {
+        case 202: return launch_quad_k<REV, CY, CZ, 2, 2>(A, st);
+        case 204: return launch_quad_k<REV, CY, CZ, 2, 4>(A, st);
+        case 402: return launch_quad_k<REV, CY, CZ, 4, 2>(A, st);
+        case 103: return launch_quad_k<REV, CY, CZ, 1, 3>(A, st);
+        default: return launch_quad_k<REV, CY, CZ, 2, 3>(A, st);
+    }
+}
+
+cudaError_t launch_mic_quad(bool rev, const LaneArgs &A, cudaStream_t st) {
+    int cy, cz;
+    quad_cluster_shape(&cy, &cz);
+    if (!A.geom.quad || A.geom.TB % cy || A.geom.TC % cz) return cudaErrorNotSupported;
+#define QCASE(a, b)                                                                          \
+    if (cy == a && cz == b) return rev ? launch_quad_c<true, a, b>(A, st) : launch_quad_c<false, a, b>(A, st);
+    QCASE(2, 4)
+    QCASE(4, 4)
+    QCASE(2, 2)
+    QCASE(4, 2)
+    QCASE(1, 4)
+    QCASE(1, 1)
+#undef QCASE
+    return cudaErrorNotSupported;
+}
+
+}  // namespace flip

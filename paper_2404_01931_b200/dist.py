@@ -1,67 +1,57 @@
 """Slab decomposition of the FLIP step over ranks (one process per GPU).
 
-SURVEY §8(e); north star: "the domain is slab-decomposed ... particle
-migration ... ghost layers ... reductions allreduced".
+SURVEY §8(e); north star: "the domain is slab-decomposed across the 8 GPUs
+of one box, with ghost-layer pressure/velocity halo exchange and particle
+migration over NVLink (NCCL or P2P), and the CG dot products are
+allreduced".
 
 Decomposition
 -------------
-Rank r owns the cell z-planes ``[k0, k1)`` of :class:`SlabPlan`.  Every grid
-array is x-fastest with z slowest (``flipsim/grid.py:47-72``), so a slab is a
-contiguous range of each cell and face array, and the particles of a slab are
-a contiguous range of the cell-sorted particle set.  Each rank holds the
-particles of its own slab, in global order, and the whole grid.
+Rank r owns the cell z-planes ``[k0, k1)`` of :class:`SlabPlan`.  The flat
+index is x-fastest with z slowest (``flipsim/grid.py:47-72``), so the rank's
+cells, the faces of its planes, the pressure rows of its cells (rows ascend
+with the cell index, ``pressure.py:76-166``) and its cell-sorted particles
+are each one contiguous range of the global arrays.  Every device array
+keeps its full-grid size and global indexing; the library computes only the
+rank's range and calls back into :class:`Transport` for each exchange
+(``flip_comm`` in ``include/flipb200.h``, driven from inside
+``flip_step``).  Per step, all on the device and stream-ordered:
 
-Per step (``flipsim/sim.py:226-300``), with the exchange that makes each
-stage exact:
+==================  ======================================================
+stage               sharding / exchange (``csrc/slab.cu``, ``pressure.cu``)
+==================  ======================================================
+dt                  own particles; MAX-allreduce of max|v|^2 (8 B)
+advect + migrate    own particles; particles whose cell left the slab go
+                    to its owner (all-to-all, order kept)
+bin, classify       own particles / own cells; the label planes are
+                    all-gathered (1 B/cell: sealed-region pinning is global)
+P2G + force         own face planes; the neighbours' boundary particle
+                    planes are the ghosts; then 1-plane face halos
+assemble            own rows' rhs (global row numbering); MAX of max|rhs|
+solve               own rows; 1-plane row halo before every stencil pass,
+                    MAX-allreduced residuals, distributed bit-exact
+                    pairwise dots; MIC(0) / GS / multigrid sweeps are
+                    global recurrences: replicated on the all-gathered r
+gradient, extrap.   own face planes; 1-plane face halos between passes
+G2P, reseed         own particles / own cells
+==================  ======================================================
 
-1. dt (``particles.py:214-224``): local, then allreduce MIN.  dt is a
-   monotone function of max|v|^2, so the MIN of the local values is the
-   global value bit for bit.
-2. advect: local.
-3. migration: particles whose cell left the slab go to the owning rank
-   (``all_to_all``).  The receive buffer is ordered by source rank, and the
-   global order is rank order, so the stable sort of step 4 reproduces the
-   1-GPU order.
-4. bin: local.
-5. classify: local (FLUID needs count > 0), then allreduce MIN of the labels
-   (SOLID 0 < FLUID 1 < AIR 2).
-6. ghost planes: each rank sends its first/last particle plane to its
-   neighbours.  P2G (``transfer.py:35-57``) of a face in the slab reads cells
-   one plane beyond it.
-7. P2G + force on [ghost_lo, own, ghost_hi], then the ghosts are dropped and
-   the slab re-binned.
-8. owned faces of grid, grid_old and the known masks are all-gathered.
-   Every rank then holds the 1-GPU grid.
-9. assemble / solve / gradient / extrapolation: replicated (see below).
-10. G2P: local.
-11. reseed: local, restricted to the slab's cells (``flip_set_slab``).
-
-The result on every rank is the 1-GPU grid, and the concatenation of the
-ranks' particles in rank order is the 1-GPU particle set, bit for bit
-(``tests/test_dist_*``).
-
-Why the solve is replicated.  Every PCG iteration applies MIC(0), a
-sequential recurrence across the whole grid (``_core.pyx:311-347``).  Its
-critical path (≈ nx + ny + nz dependent hyperplanes) does not shorten when
-split over GPUs.  The pipelined wavefront could cross slab boundaries over
-peer memory, but each such boundary adds NVLink latency to that path.
-Splitting only the vector kernels (≈ 20% of the solve) would need a
-distributed pairwise-dot tree and per-iteration halo exchanges for a
-fraction of the step.  The replicated solve keeps the reference's
-arithmetic and costs no communication.  The particle-side stages are the
-part that scales.
+The concatenation of the ranks' particles (rank order) is the 1-GPU particle
+array and every rank's own planes hold the 1-GPU grid, bit for bit
+(``tests/test_dist_gpu.py``).
 
 Transport
 ---------
-Exchanges run on torch tensors that alias the ctx's device buffers:
-``backend="nccl"`` uses them directly, ``"gloo"`` stages through host memory
-(CPU tests, or two ranks sharing one GPU with no cross-process waits in any
-kernel).
+``backend="nccl"``: collectives on the ctx stream (``torch.cuda.ExternalStream``)
+over device tensors aliasing the ctx's buffers, no host sync.  ``"gloo"``:
+staged through host memory (CPU tests; ranks sharing the one GPU of this
+pool, where no kernel waits on another process).
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import traceback
 from dataclasses import dataclass
 
 import numpy as np
@@ -71,8 +61,10 @@ from ._lib import LIB, check
 from . import rng
 from . import sim as _sim
 
-__all__ = ["SlabPlan", "Transport", "make_scene", "step", "gather_particles",
-           "migrate_rows", "ghost_rows", "face_ranges"]
+__all__ = ["SlabPlan", "Transport", "make_scene", "step", "gather_particles", "gather_grid",
+           "face_ranges", "pairwise_tree_plan", "distributed_pairwise_sum", "exchange_stats"]
+
+FLIP_OP_MAX, FLIP_OP_MIN, FLIP_OP_SUM = 0, 1, 2
 
 
 # ----------------------------------------------------------------- plan ----
@@ -90,6 +82,9 @@ class SlabPlan:
 
     def planes(self, rank: int) -> tuple:
         return (rank * self.nz) // self.world, ((rank + 1) * self.nz) // self.world
+
+    def starts(self) -> list:
+        return [self.planes(r)[0] for r in range(self.world)] + [self.nz]
 
     def owner_of_plane(self, k: int) -> int:
         for r in range(self.world):
@@ -114,7 +109,7 @@ class SlabPlan:
 def face_ranges(plan: SlabPlan, comp: int, rank: int) -> tuple:
     """[lo, hi) flat indices of the faces of component ``comp`` that rank
     owns: the faces of its cell planes, plus the top w plane (k = nz) on the
-    last rank (``grid.py:65-72`` layouts)."""
+    last rank (``grid.py:65-72`` layouts; ``slab_face_range`` in slab.cu)."""
     k0, k1 = plan.planes(rank)
     nx, ny = plan.nx, plan.ny
     if comp == 0:
@@ -128,10 +123,128 @@ def face_ranges(plan: SlabPlan, comp: int, rank: int) -> tuple:
     return k0 * per, k1 * per
 
 
+# ------------------------------------- distributed pairwise tree (mirror) ---
+def _split(n: int) -> int:
+    n2 = n // 2
+    return n2 - n2 % 8
+
+
+def _pairwise(a) -> float:
+    """numpy DOUBLE_pairwise_sum (np.add.reduce, pressure.py:269-271)."""
+    n = len(a)
+    if n < 8:
+        s = 0.0
+        for v in a:
+            s += float(v)
+        return s
+    if n <= 128:
+        r = [float(a[i]) for i in range(8)]
+        for i in range(8, n - n % 8, 8):
+            for k in range(8):
+                r[k] += float(a[i + k])
+        s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        for i in range(n - n % 8, n):
+            s += float(a[i])
+        return s
+    n2 = _split(n)
+    return _pairwise(a[:n2]) + _pairwise(a[n2:])
+
+
+def pairwise_tree_plan(n: int):
+    """(cut, node spans) of the deepest tree level at which every node
+    exists (pw_cut in pressure.cu)."""
+    spans = [(0, n)]
+    cut = 0
+    while spans and all(l > 128 for _, l in spans):
+        nxt = []
+        for s, l in spans:
+            n2 = _split(l)
+            nxt += [(s, n2), (s + n2, l - n2)]
+        spans = nxt
+        cut += 1
+    return cut, spans
+
+
+def distributed_pairwise_sum(parts) -> float:
+    """Host restatement of the slab dot (launch_dot_slab, pressure.cu):
+    ``parts`` are the ranks' contiguous pieces of one vector.  Each rank sums
+    the cut-level nodes that start in its rows (reading the next ranks'
+    leading elements), reduces them to maximal aligned blocks, and the
+    blocks are merged in index order -- bit-identical to np.add.reduce of the
+    concatenation (tests/test_dist_host.py)."""
+    full = np.concatenate(parts) if parts else np.zeros(0)
+    n = len(full)
+    cut, spans = pairwise_tree_plan(max(n, 1))
+    starts = np.cumsum([0] + [len(p) for p in parts])
+    blocks = []
+    for q in range(len(parts)):
+        r0, r1 = int(starts[q]), int(starts[q + 1])
+        mine = [k for k, (s, _) in enumerate(spans) if r0 <= s < r1 or (q == len(parts) - 1 and s >= r1)]
+        if n == 0 or not mine:
+            continue
+        na, nb = mine[0], mine[-1] + 1
+        v = {k: _pairwise(full[spans[k][0]:spans[k][0] + spans[k][1]]) for k in range(na, nb)}
+        st = 1
+        while st < nb - na:
+            for g in range(na, nb):
+                if g % (2 * st) == 0 and g + 2 * st <= nb:
+                    v[g] = v[g] + v[g + st]
+            st *= 2
+        g = na
+        while g < nb:
+            lvl = 0
+            while (g >> lvl) & 1 == 0 and g + (2 << lvl) <= nb:
+                lvl += 1
+            blocks.append((lvl, g >> lvl, v[g]))
+            g += 1 << lvl
+    stack = []
+    for b in blocks:
+        stack.append(list(b))
+        while (len(stack) >= 2 and stack[-1][0] == stack[-2][0] and stack[-2][1] % 2 == 0
+               and stack[-1][1] == stack[-2][1] + 1):
+            top = stack.pop()
+            stack[-1] = [top[0] + 1, stack[-1][1] >> 1, stack[-1][2] + top[2]]
+    return stack[0][2] if stack else 0.0
+
+
 # ------------------------------------------------------------ transport ----
+_NEIGH = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                     C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64)
+_ALLRED = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32)
+_ALLGV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64))
+_A2AV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
+                    C.c_void_p, C.POINTER(C.c_int64))
+
+
+class FlipComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("neighbors", _NEIGH), ("allreduce", _ALLRED),
+                ("allgatherv", _ALLGV), ("alltoallv", _A2AV)]
+
+
+class _CAI:
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _dview(ptr, nbytes: int, typestr: str = "|u1", itemsize: int = 1):
+    """A torch tensor aliasing device memory (no copy)."""
+    import torch
+    n = int(nbytes) // itemsize
+    if n == 0 or not ptr:
+        return torch.empty(0, dtype={"|u1": torch.uint8, "<i8": torch.int64}[typestr],
+                           device="cuda")
+    return torch.as_tensor(_CAI(ptr, n, typestr), device="cuda")
+
+
 class Transport:
-    """torch.distributed collectives on device tensors (NCCL) or staged
-    through host memory (gloo)."""
+    """The flip_comm callbacks over torch.distributed.
+
+    Each collective also has a tensor-level form (``*_t``) used directly by
+    the CPU tests.  With NCCL the tensors are device views and the ops run
+    on the library's stream; with gloo they are staged through host memory
+    (the stream is synchronised first and the results copied back before
+    the callback returns)."""
 
     def __init__(self, group=None):
         import torch
@@ -142,19 +255,125 @@ class Transport:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.staged = dist.get_backend(group) != "nccl"
+        self._cbs = None
 
-    def _out(self, t):
-        return t.cpu() if self.staged else t
+    # ---- tensor level -------------------------------------------------
+    def neighbors_t(self, send_lo, send_hi, recv_lo, recv_hi):
+        """send_lo -> rank-1, send_hi -> rank+1; recv_lo <- rank-1,
+        recv_hi <- rank+1 (empty tensors skip)."""
+        d, ops = self.dist, []
+        r, w = self.rank, self.world
+        if r > 0 and send_lo.numel():
+            ops.append(d.P2POp(d.isend, send_lo, r - 1, self.group))
+        if r > 0 and recv_lo.numel():
+            ops.append(d.P2POp(d.irecv, recv_lo, r - 1, self.group))
+        if r + 1 < w and send_hi.numel():
+            ops.append(d.P2POp(d.isend, send_hi, r + 1, self.group))
+        if r + 1 < w and recv_hi.numel():
+            ops.append(d.P2POp(d.irecv, recv_hi, r + 1, self.group))
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
 
-    def _back(self, t, like):
-        return t.to(like.device) if self.staged else t
+    def allreduce_t(self, t, op: int):
+        d = self.dist
+        red = {FLIP_OP_MAX: d.ReduceOp.MAX, FLIP_OP_MIN: d.ReduceOp.MIN,
+               FLIP_OP_SUM: d.ReduceOp.SUM}[int(op)]
+        d.all_reduce(t, op=red, group=self.group)
 
-    def allreduce_min_(self, t):
-        x = self._out(t)
-        self.dist.all_reduce(x, op=self.dist.ReduceOp.MIN, group=self.group)
-        if self.staged:
-            t.copy_(x)
-        return t
+    def allgatherv_t(self, buf, offsets):
+        """In place: bytes [offsets[q], offsets[q+1]) of rank q everywhere."""
+        torch = self.torch
+        sizes = [int(offsets[q + 1] - offsets[q]) for q in range(self.world)]
+        m = max(max(sizes), 1)
+        mine = torch.zeros(m, dtype=buf.dtype, device=buf.device)
+        a, b = int(offsets[self.rank]), int(offsets[self.rank + 1])
+        mine[:b - a] = buf[a:b]
+        out = torch.empty(m * self.world, dtype=buf.dtype, device=buf.device)
+        self.dist.all_gather_into_tensor(out, mine, group=self.group)
+        for q in range(self.world):
+            if q != self.rank and sizes[q]:
+                buf[int(offsets[q]):int(offsets[q + 1])] = out[q * m:q * m + sizes[q]]
+
+    def alltoallv_t(self, send, sbytes, recv, rbytes):
+        self.dist.all_to_all_single(recv, send, [int(x) for x in rbytes],
+                                    [int(x) for x in sbytes], group=self.group)
+
+    # ---- flip_comm callbacks (device pointers) -------------------------
+    def _stage(self, views):
+        """gloo: host copies of device views (after the ctx stream drained)."""
+        return [v.cpu() for v in views]
+
+    def _run(self, stream, fn):
+        torch = self.torch
+        try:
+            if self.staged:
+                torch.cuda.synchronize()
+                fn()
+                torch.cuda.synchronize()
+            else:
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0))):
+                    fn()
+            return 0
+        except Exception:  # reported through the C status
+            traceback.print_exc()
+            return 1
+
+    def comm(self) -> FlipComm:
+        """The callback table for flip_set_slab_comm (kept alive here)."""
+        if self._cbs is not None:
+            return self._cbs[0]
+
+        def neighbors(user, stream, slo, nslo, shi, nshi, rlo, nrlo, rhi, nrhi):
+            def go():
+                views = [_dview(slo, nslo), _dview(shi, nshi), _dview(rlo, nrlo), _dview(rhi, nrhi)]
+                if self.staged:
+                    h = self._stage(views)
+                    self.neighbors_t(*h)
+                    views[2].copy_(h[2])
+                    views[3].copy_(h[3])
+                else:
+                    self.neighbors_t(*views)
+            return self._run(stream, go)
+
+        def allreduce(user, stream, buf, n, op):
+            def go():
+                v = _dview(buf, 8 * n, "<i8", 8)
+                t = v.cpu() if self.staged else v
+                self.allreduce_t(t, op)
+                if self.staged:
+                    v.copy_(t)
+            return self._run(stream, go)
+
+        def allgatherv(user, stream, buf, offsets):
+            def go():
+                off = [int(offsets[q]) for q in range(self.world + 1)]
+                v = _dview(buf, off[-1])
+                t = v.cpu() if self.staged else v
+                self.allgatherv_t(t, off)
+                if self.staged:
+                    v.copy_(t)
+            return self._run(stream, go)
+
+        def alltoallv(user, stream, send, sbytes, recv, rbytes):
+            def go():
+                sb = [int(sbytes[q]) for q in range(self.world)]
+                rb = [int(rbytes[q]) for q in range(self.world)]
+                s, r = _dview(send, sum(sb)), _dview(recv, sum(rb))
+                if self.staged:
+                    hs = s.cpu()
+                    hr = self.torch.empty(sum(rb), dtype=self.torch.uint8)
+                    self.alltoallv_t(hs, sb, hr, rb)
+                    if sum(rb):
+                        r.copy_(hr)
+                else:
+                    self.alltoallv_t(s, sb, r, rb)
+            return self._run(stream, go)
+
+        fns = (_NEIGH(neighbors), _ALLRED(allreduce), _ALLGV(allgatherv), _A2AV(alltoallv))
+        cs = FlipComm(None, *fns)
+        self._cbs = (cs, fns)
+        return cs
 
     def allreduce_sum_int(self, v: int) -> int:
         t = self.torch.tensor([int(v)], dtype=self.torch.int64)
@@ -163,252 +382,110 @@ class Transport:
         self.dist.all_reduce(t, group=self.group)
         return int(t.item())
 
-    def all_to_all_rows(self, rows, send_counts):
-        """rows: (n, k) grouped by destination rank in rank order; returns the
-        received rows grouped by source rank in rank order, and the counts."""
-        torch = self.torch
-        sc = torch.tensor([int(c) for c in send_counts], dtype=torch.int64)
-        rc = torch.empty(self.world, dtype=torch.int64)
-        if not self.staged:
-            sc, rc = sc.cuda(), rc.cuda()
-        self.dist.all_to_all_single(rc, sc, group=self.group)
-        recv_counts = [int(c) for c in rc.tolist()]
-        k = rows.shape[1]
-        src = self._out(rows.contiguous())
-        dst = torch.empty((sum(recv_counts), k), dtype=rows.dtype, device=src.device)
-        self.dist.all_to_all_single(dst.view(-1), src.view(-1),
-                                    [c * k for c in recv_counts],
-                                    [int(c) * k for c in send_counts], group=self.group)
-        return self._back(dst, rows), recv_counts
-
-    def allgather_var(self, local, sizes):
-        """all-gather of 1-D tensors of per-rank lengths ``sizes``."""
-        torch = self.torch
-        m = max(max(sizes), 1)
-        x = self._out(local)
-        pad = torch.zeros(m, dtype=x.dtype, device=x.device)
-        pad[:x.numel()] = x
-        parts = [torch.empty(m, dtype=x.dtype, device=x.device) for _ in range(self.world)]
-        self.dist.all_gather(parts, pad, group=self.group)
-        return [self._back(p[:s], local) for p, s in zip(parts, sizes)]
-
-
-# ------------------------------------------------- host-logic pieces ----
-def migrate_rows(rows, plane_of_row, owners, tr: Transport):
-    """Send each row to the rank owning its z-plane.  ``rows`` (n, k) in the
-    rank's current order; returns the rows this rank now owns, in global
-    order (source ranks ascending, each source's order kept)."""
-    torch = tr.torch
-    dest = owners[plane_of_row.long()]
-    order = torch.argsort(dest, stable=True)
-    counts = torch.bincount(dest, minlength=tr.world).tolist()
-    return tr.all_to_all_rows(rows[order], counts)[0]
-
-
-def ghost_rows(rows, first_plane, last_plane, tr: Transport):
-    """Exchange boundary planes with the neighbours.  ``first_plane`` /
-    ``last_plane`` are (start, end) row ranges of the rank's first and last
-    cell plane in ``rows``.  Returns (ghost_lo, ghost_hi): the previous
-    rank's last plane and the next rank's first plane."""
-    torch = tr.torch
-    r, w = tr.rank, tr.world
-    parts, counts = [], [0] * w
-    if r > 0:
-        parts.append(rows[first_plane[0]:first_plane[1]])
-        counts[r - 1] = first_plane[1] - first_plane[0]
-    if r + 1 < w:
-        parts.append(rows[last_plane[0]:last_plane[1]])
-        counts[r + 1] = last_plane[1] - last_plane[0]
-    send = torch.cat(parts) if parts else rows[:0]
-    recv, rc = tr.all_to_all_rows(send, counts)
-    nlo = rc[r - 1] if r > 0 else 0
-    return recv[:nlo], recv[nlo:]
-
-
-# ------------------------------------------------------- device views ----
-class _CAI:
-    def __init__(self, ptr: int, n: int, typestr: str):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
-                                         "data": (int(ptr), False), "version": 3}
-
-
-def _view(ptr, n: int, dtype):
-    import torch
-    typestr = {torch.float64: "<f8", torch.int32: "<i4", torch.uint8: "|u1"}[dtype]
-    if n == 0:
-        return torch.empty(0, dtype=dtype, device="cuda")
-    return torch.as_tensor(_CAI(ptr, n, typestr), device="cuda")
-
-
-def _ptrs(dev):
-    p = _lib.DevPtrs()
-    check(LIB.flip_get_dev_ptrs(dev.ctx, C.byref(p)), "flip_get_dev_ptrs")
-    return p
-
-
-def _particle_rows(dev):
-    import torch
-    p = _ptrs(dev)
-    n = int(p.n)
-    cols = [_view(p.pos[a], n, torch.float64) for a in range(3)]
-    cols += [_view(p.vel[a], n, torch.float64) for a in range(3)]
-    return torch.stack(cols, dim=1) if n else torch.empty((0, 6), dtype=torch.float64, device="cuda")
-
-
-def _write_particles(dev, rows) -> None:
-    import torch
-    p = _ptrs(dev)
-    m = int(rows.shape[0])
-    torch.cuda.synchronize()
-    if m > p.capacity:  # grow first (keeps nothing we need: rows is a copy)
-        check(LIB.flip_reserve_particles(dev.ctx, m), "flip_reserve_particles")
-        p = _ptrs(dev)
-    for a in range(6):
-        ptr = p.pos[a] if a < 3 else p.vel[a - 3]
-        if m:
-            _view(ptr, m, torch.float64).copy_(rows[:, a])
-    torch.cuda.synchronize()
-    check(LIB.flip_set_particle_count(dev.ctx, m), "flip_set_particle_count")
-    dev.bump()
-
-
-def _particle_planes(dev, plan: SlabPlan):
-    import torch
-    n = dev.count()
-    cells = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
-    check(LIB.flip_particle_cells(dev.ctx, C.c_void_p(cells.data_ptr())), "flip_particle_cells")
-    check(LIB.flip_synchronize(dev.ctx))
-    return (cells[:n].long() // plan.plane_cells)
+    def allgather_obj(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
 
 
 # ---------------------------------------------------------- the step ----
 class SlabContext:
     def __init__(self, plan: SlabPlan, tr: Transport):
-        import torch
         self.plan = plan
         self.tr = tr
-        self.owners = torch.as_tensor(plan.plane_owners(), device="cuda")
 
 
 def make_scene(spec, rng_seed: int = 0, group=None, device: int = 0, capacity: int = 0):
     """make_scene on every rank (the scene builder is deterministic), then
-    each rank keeps the particles of its own slab."""
+    each rank keeps the particles of its own planes (a contiguous range of
+    the binned set) and enters slab mode."""
+    import torch
+    if getattr(spec, "advection", "euler") != "euler":
+        raise _sim.ConfigError("RK2 advection is not supported with a slab decomposition")
     tr = Transport(group)
     state = _sim.make_scene(spec, rng_seed, device=device, capacity=capacity)
     dev = state.device
     plan = SlabPlan(dev.dims.nx, dev.dims.ny, dev.dims.nz, tr.world)
-    ctx = SlabContext(plan, tr)
     k0, k1 = plan.planes(tr.rank)
-    check(LIB.flip_set_slab(dev.ctx, k0, k1), "flip_set_slab")
-    planes = _particle_planes(dev, plan)
-    rows = _particle_rows(dev)
-    keep = (planes >= k0) & (planes < k1)
-    _write_particles(dev, rows[keep])
+    pc = plan.plane_cells
+    p = _lib.DevPtrs()
+    check(LIB.flip_get_dev_ptrs(dev.ctx, C.byref(p)), "flip_get_dev_ptrs")
+    off, _cnt = dev.hash_arrays()
+    a = int(off[k0 * pc])
+    b = int(off[k1 * pc]) if k1 * pc < len(off) else int(p.n)
+    torch.cuda.synchronize()
+    for ptr in list(p.pos) + list(p.vel):
+        v = _dview(ptr, 8 * int(p.n), "<i8", 8)
+        keep = v[a:b].clone()
+        v[:b - a].copy_(keep)
+    torch.cuda.synchronize()
+    check(LIB.flip_set_particle_count(dev.ctx, b - a), "flip_set_particle_count")
+    dev.bump()
     rc, _ = dev.run_stages(_sim._params(spec, dev.dims.dtau), _lib.STAGE["bin"], _lib.STAGE["bin"])
     check(rc, "slab bin")
-    state.slab = ctx
+    starts = (C.c_int64 * (tr.world + 1))(*plan.starts())
+    comm = tr.comm()
+    check(LIB.flip_set_slab_comm(dev.ctx, tr.rank, tr.world, C.addressof(starts),
+                                 C.addressof(comm)), "flip_set_slab_comm")
+    state.slab = SlabContext(plan, tr)
     return state
 
 
-def _stages(state, params, first: str, last: str, acc: dict):
-    dev = state.device
-    rc, rep = dev.run_stages(params, _lib.STAGE[first], _lib.STAGE[last])
-    if rc in (_lib.FLIP_E_SINGULAR, _lib.FLIP_E_BREAKDOWN):
-        _sim._raise_solver(state, rep)
-    check(rc, f"flip_run_stages {first}..{last}")
-    for i in range(_lib.STAGE[first], _lib.STAGE[last] + 1):
-        name = _lib.STAGE_NAMES[i]
-        acc[name] = acc.get(name, 0.0) + float(rep.stage_ms[i])
-    acc["_launches"] = acc.get("_launches", 0) + int(rep.gpu_launches)
-    return rep
-
-
 def step(state, cfg):
-    """One slab-decomposed timestep; same StepReport as ``sim.step``."""
-    import torch
-    ctx: SlabContext = state.slab
-    plan, tr = ctx.plan, ctx.tr
+    """One slab-decomposed timestep (the whole step runs inside
+    flip_step); same StepReport as ``sim.step`` with the global particle
+    count."""
     dev = state.device
+    tr = state.slab.tr
     seed = rng.derive_seed(state.rng_seed, state.step_count + 1)
     params = _sim._params(cfg, dev.dims.dtau, seed)
-    acc: dict = {}
-    k0, k1 = plan.planes(tr.rank)
-    pc = plan.plane_cells
-
-    # 1. dt: local, allreduce MIN
-    _stages(state, params, "dt_compute", "dt_compute", acc)
-    dt = torch.tensor([dev.dt()], dtype=torch.float64, device="cuda")
-    tr.allreduce_min_(dt)
-    dev.set_dt(float(dt.item()))
-    # 2-3. advect, migration
-    _stages(state, params, "advect", "advect", acc)
-    rows = migrate_rows(_particle_rows(dev), _particle_planes(dev, plan), ctx.owners, tr)
-    _write_particles(dev, rows)
-    # 4-5. bin, classify + label MIN
-    _stages(state, params, "bin", "classify", acc)
-    p = _ptrs(dev)
-    label = _view(p.label, dev.dims.ncells, torch.uint8)
-    tr.allreduce_min_(label)
-    torch.cuda.synchronize()
-    # 6. ghost planes
-    offset = _view(p.offset, dev.dims.ncells + 1, torch.int32)
-    bounds = offset[torch.tensor([k0 * pc, (k0 + 1) * pc, (k1 - 1) * pc, k1 * pc],
-                                 device="cuda")].tolist()
-    own = _particle_rows(dev)
-    n_own = int(own.shape[0])
-    glo, ghi = ghost_rows(own, (bounds[0], bounds[1]), (bounds[2], bounds[3]), tr)
-    _write_particles(dev, torch.cat([glo, own, ghi]))
-    # 7. bin the extended set, P2G + force, drop the ghosts, re-bin
-    _stages(state, params, "bin", "bin", acc)
-    _stages(state, params, "p2g", "force", acc)
-    _write_particles(dev, own)
-    _stages(state, params, "bin", "bin", acc)
-    # 8. owned faces of grid, grid_old, known masks
-    p = _ptrs(dev)
-    nfaces = dev.nfaces
-    arrays = [(p.u, 0, torch.float64), (p.v, 1, torch.float64), (p.w, 2, torch.float64),
-              (p.uo, 0, torch.float64), (p.vo, 1, torch.float64), (p.wo, 2, torch.float64),
-              (p.ku, 0, torch.uint8), (p.kv, 1, torch.uint8), (p.kw, 2, torch.uint8)]
-    for ptr, comp, dtype in arrays:
-        full = _view(ptr, nfaces[comp], dtype)
-        rngs = [face_ranges(plan, comp, r) for r in range(tr.world)]
-        lo, hi = rngs[tr.rank]
-        parts = tr.allgather_var(full[lo:hi], [b - a for a, b in rngs])
-        for r, (a, b) in enumerate(rngs):
-            if r != tr.rank and b > a:
-                full[a:b].copy_(parts[r])
-    torch.cuda.synchronize()
-    dev.bump()
-    # 9-11. replicated grid stages, then G2P + reseed on the slab
-    rep = _stages(state, params, "project", "apply_gradient", acc)
-    solver = (int(rep.solver_iterations), float(rep.solver_residual), bool(rep.solver_converged),
-              int(rep.nrows), int(rep.npinned))
-    rep2 = _stages(state, params, "g2p", "reseed", acc)
-    total = tr.allreduce_sum_int(int(rep2.particle_count))
-    timings = _sim.StageTimings(**{n: acc.get(n, 0.0) for n in _lib.STAGE_NAMES})
-    state.time += float(dt.item())
+    rc, rep = dev.run_stages(params, 0, _lib.NSTAGES - 1)
+    if rc in (_lib.FLIP_E_SINGULAR, _lib.FLIP_E_BREAKDOWN):
+        _sim._raise_solver(state, rep)
+    check(rc, "flip_step (slab)")
+    total = tr.allreduce_sum_int(int(rep.particle_count))
+    timings = _sim.StageTimings(**{n: float(rep.stage_ms[i])
+                                   for i, n in enumerate(_lib.STAGE_NAMES)})
+    state.time += float(rep.dt)
     state.step_count += 1
-    return _sim.StepReport(timings=timings, dt=float(dt.item()), particle_count=total,
-                           solver_iterations=solver[0], solver_residual=solver[1],
-                           solver_converged=solver[2], nrows=solver[3], npinned=solver[4],
-                           gpu_launches=int(acc["_launches"]))
+    return _sim.StepReport(timings=timings, dt=float(rep.dt), particle_count=total,
+                           solver_iterations=int(rep.solver_iterations),
+                           solver_residual=float(rep.solver_residual),
+                           solver_converged=bool(rep.solver_converged), nrows=int(rep.nrows),
+                           npinned=int(rep.npinned), gpu_launches=int(rep.gpu_launches))
+
+
+def exchange_stats(state) -> dict:
+    """Bytes this rank sent and collective calls since the last query."""
+    sent, calls = C.c_int64(0), C.c_int64(0)
+    check(LIB.flip_slab_bytes(state.device.ctx, C.byref(sent), C.byref(calls)))
+    return {"bytes_sent": int(sent.value), "calls": int(calls.value)}
 
 
 def gather_particles(state):
     """The global particle set (host arrays, every rank), concatenated in
     rank order = the 1-GPU order."""
-    import torch
     tr: Transport = state.slab.tr
-    rows = _particle_rows(state.device)
-    sizes = [0] * tr.world
-    n = torch.tensor([rows.shape[0]], dtype=torch.int64)
-    if not tr.staged:
-        n = n.cuda()
-    lst = [torch.zeros_like(n) for _ in range(tr.world)]
-    tr.dist.all_gather(lst, n, group=tr.group)
-    sizes = [int(x.item()) for x in lst]
-    cols = []
-    for a in range(6):
-        parts = tr.allgather_var(rows[:, a].contiguous(), sizes)
-        cols.append(torch.cat(parts).cpu().numpy())
-    return tuple(cols)
+    parts = state.particles.arrays()
+    allp = tr.allgather_obj([np.asarray(a) for a in parts])
+    return tuple(np.concatenate([allp[q][a] for q in range(tr.world)]) for a in range(6))
+
+
+def gather_grid(state):
+    """The global grid / grid_old / hash as one GPU holds them: every array
+    assembled from its owners' planes (host arrays, every rank)."""
+    tr: Transport = state.slab.tr
+    plan = state.slab.plan
+    g, go = state.grid, state.grid_old
+    pc = plan.plane_cells
+    k0, k1 = plan.planes(tr.rank)
+    mine = {}
+    for name, arr in (("u", g.u), ("v", g.v), ("w", g.w), ("uo", go.u), ("vo", go.v),
+                      ("wo", go.w)):
+        comp = "uvw".index(name[0])
+        a, b = face_ranges(plan, comp, tr.rank)
+        mine[name] = np.asarray(arr)[a:b]
+    for name, arr in (("p", g.p), ("label", g.label), ("count", state.hash.count)):
+        mine[name] = np.asarray(arr)[k0 * pc:k1 * pc]
+    every = tr.allgather_obj(mine)
+    return {k: np.concatenate([every[q][k] for q in range(tr.world)]) for k in mine}

@@ -1,7 +1,7 @@
 """Worker for tests/test_dist_gpu.py: the slab-decomposed step on ranks that
 share one GPU, exchanging through gloo (host-staged; no kernel waits on
 another process).  Rank 0 writes digests of the gathered state after every
-step to argv[1]."""
+step, and every rank's exchange volume, to argv[1]."""
 import hashlib
 import json
 import os
@@ -28,19 +28,22 @@ def main():
     torch.cuda.set_device(0)
     spec = P.SceneSpec(**case["spec"])
     st = D.make_scene(spec, rng_seed=case["seed"])
-    recs = []
+    recs, xfer = [], []
     for _ in range(case["steps"]):
         rep = D.step(st, spec)
+        xfer.append(D.exchange_stats(st))
         parts = D.gather_particles(st)
-        g, go = st.grid, st.grid_old
+        g = D.gather_grid(st)
         rec = {f"part{i}": digest(a) for i, a in enumerate(parts)}
-        rec.update({k: digest(getattr(g, k)) for k in ("u", "v", "w", "p", "label")})
-        rec.update({"uo": digest(go.u), "vo": digest(go.v), "wo": digest(go.w)})
+        rec.update({k: digest(g[k]) for k in ("u", "v", "w", "p", "label", "uo", "vo", "wo")})
+        rec["count"] = digest(g["count"].astype(np.int64))
         rec.update({"n": int(rep.particle_count), "dt": float(rep.dt).hex(),
-                    "its": int(rep.solver_iterations), "res": float(rep.solver_residual).hex()})
+                    "its": int(rep.solver_iterations), "res": float(rep.solver_residual).hex(),
+                    "conv": bool(rep.solver_converged), "nrows": int(rep.nrows)})
         recs.append(rec)
+    every = st.slab.tr.allgather_obj(xfer)
     if dist.get_rank() == 0:
-        json.dump(recs, open(out_path, "w"))
+        json.dump({"steps": recs, "exchange": every}, open(out_path, "w"))
     print(f"rank {dist.get_rank()} ok", flush=True)
     dist.destroy_process_group()
 

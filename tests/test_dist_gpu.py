@@ -1,6 +1,11 @@
-"""Slab-decomposed step (paper_2404_01931_b200/dist.py) vs the 1-GPU step:
-2 and 3 ranks sharing the one GPU, gloo transport.  Particles gathered in
-rank order, grid, grid_old and the StepReport must be bit-identical."""
+"""Slab-decomposed step (paper_2404_01931_b200/dist.py, csrc/slab.cu) vs the
+1-GPU step: 2 and 3 ranks sharing the one GPU, gloo transport.  Every stage
+runs on the rank's planes / rows / particles; the particles gathered in rank
+order, the grid, grid_old and hash assembled from the owners' planes, and
+the StepReport must be bit-identical, for every solver (Jacobi, RBGS and
+PCG with Jacobi / no preconditioner are sharded with row halos and the
+distributed pairwise dot; MIC(0), GS and multigrid run their sweeps
+replicated)."""
 import hashlib
 import json
 import os
@@ -17,8 +22,17 @@ CASES = [
     dict(spec=dict(name="dam-break", res=16, solver="pcg"), seed=3, steps=3),
     dict(spec=dict(name="double-dam-break", res=20, solver="jacobi"), seed=1, steps=2),
     dict(spec=dict(name="water-drop", res=16, solver="pcg"), seed=2, steps=3),
-    # larger: several clusters in the sweep, heavy slab-crossing migration
+    dict(spec=dict(name="double-dam-break", res=18, solver="rbgs"), seed=4, steps=3),
+    dict(spec=dict(name="dam-break", res=20, solver="pcg", precond="jacobi"), seed=5, steps=3),
+    dict(spec=dict(name="water-drop", res=18, solver="pcg", precond="none",
+                   flip_fraction=0.0), seed=6, steps=3),
+    dict(spec=dict(name="water-drop", res=16, solver="gs"), seed=7, steps=2),
+    dict(spec=dict(name="double-dam-break-obstacle", res=24, solver="pcg", precond="mg"),
+         seed=8, steps=2),
+    # larger: several clusters in the sweep, heavy slab-crossing migration,
+    # thousands of rows per rank (multi-level distributed dot)
     dict(spec=dict(name="dam-break", res=64, solver="pcg"), seed=0, steps=4),
+    dict(spec=dict(name="dam-break", res=48, solver="pcg", precond="jacobi"), seed=0, steps=3),
 ]
 
 
@@ -46,8 +60,10 @@ def _single(case):
         rec = {f"part{i}": digest(a) for i, a in enumerate(st.particles.arrays())}
         rec.update({k: digest(getattr(g, k)) for k in ("u", "v", "w", "p", "label")})
         rec.update({"uo": digest(go.u), "vo": digest(go.v), "wo": digest(go.w)})
+        rec["count"] = digest(np.asarray(st.hash.count, dtype=np.int64))
         rec.update({"n": int(rep.particle_count), "dt": float(rep.dt).hex(),
-                    "its": int(rep.solver_iterations), "res": float(rep.solver_residual).hex()})
+                    "its": int(rep.solver_iterations), "res": float(rep.solver_residual).hex(),
+                    "conv": bool(rep.solver_converged), "nrows": int(rep.nrows)})
         recs.append(rec)
     st.device.close()
     return recs
@@ -66,9 +82,15 @@ def test_slab_step_matches_single_gpu(tmp_path, world, ci):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    got = json.load(open(out))
+    res = json.load(open(out))
+    got = res["steps"]
     exp = _single(case)
     assert len(got) == len(exp)
     for s, (g, e) in enumerate(zip(got, exp)):
         bad = [k for k in e if g[k] != e[k]]
         assert not bad, f"step {s + 1}: {bad}"
+    # every rank exchanged something every step (halos, dots, migration)
+    for r, steps in enumerate(res["exchange"]):
+        assert all(x["bytes_sent"] > 0 and x["calls"] > 0 for x in steps), (r, steps)
+    print(f"exchange per step (rank: bytes sent, calls): "
+          f"{[(r, steps[-1]['bytes_sent'], steps[-1]['calls']) for r, steps in enumerate(res['exchange'])]}")
