@@ -67,6 +67,7 @@ struct Slab {
     int64_t mig_cap = 0;
     int64_t *cnt_dev = nullptr;    // world x world counts / small scalars
     double *dotbuf = nullptr;      // distributed dot scratch (pressure.cu)
+    int *gscan = nullptr;          // ghost planes' count prefix sums (2 x nx*ny + 16)
     size_t dotcap = 0;
     int64_t bytes = 0, calls = 0;  // exchange accounting (flip_slab_bytes)
 };

@@ -56,11 +56,11 @@ int slab_allgatherv(Ctx &c, void *buf, const int64_t *offsets) {
 char *slab_xbuf(Ctx &c, size_t bytes) {
     Slab &S = c.slab;
     if (bytes > S.xcap) {
+        const size_t cap = std::max<size_t>(bytes, 2 * S.xcap);
         cudaStreamSynchronize(c.st);
         cudaFree(S.xbuf);
         S.xbuf = nullptr;
         S.xcap = 0;
-        size_t cap = std::max<size_t>(bytes, 2 * S.xcap);
         if (cudaMalloc(&S.xbuf, cap) != cudaSuccess) return nullptr;
         S.xcap = cap;
     }
@@ -74,6 +74,8 @@ int slab_free(Ctx &c) {
     if (S.kstart_dev) cudaFree(S.kstart_dev);
     if (S.cnt_dev) cudaFree(S.cnt_dev);
     if (S.dotbuf) cudaFree(S.dotbuf);
+    if (S.gscan) cudaFree(S.gscan);
+    S.gscan = nullptr;
     S.dotbuf = nullptr;
     S.dotcap = 0;
     S.xbuf = nullptr;
@@ -328,10 +330,9 @@ int slab_ghosts(Ctx &c) {
     if (int rc = slab_neighbors(c, c.count + S.k0 * pc, 4 * pc, c.count + (S.k1 - 1) * pc, 4 * pc,
                                 c.count + (S.k0 - 1) * pc, 4 * pc, c.count + S.k1 * pc, 4 * pc))
         return rc;
-    // (2) sizes: what I send (own offsets) and what I got (received counts)
-    int *tmp = (int *)slab_xbuf(c, 8 * (2 * pc + 16));
-    if (!tmp) return comm_fail("staging buffer allocation");
-    int *scan_lo = tmp, *scan_hi = tmp + pc, *tot = tmp + 2 * pc;
+    // (2) sizes: what I send (own offsets) and what I got (received counts);
+    // the ghost planes' prefix sums live in a buffer of their own (gscan)
+    int *scan_lo = S.gscan, *scan_hi = S.gscan + pc, *tot = S.gscan + 2 * pc;
     FLIP_CUDA_OK(cudaMemsetAsync(tot, 0, 8 * sizeof(int), st));
     if (has_lo) exclusive_scan(ArrayIn{c.count + (S.k0 - 1) * pc}, pc, scan_lo, tot, c.scan_tmp, st);
     if (has_hi) exclusive_scan(ArrayIn{c.count + S.k1 * pc}, pc, scan_hi, tot + 1, c.scan_tmp, st);
@@ -352,17 +353,9 @@ int slab_ghosts(Ctx &c) {
     }
     // (4) payload: 6 SoA arrays per plane, staged
     const int64_t pay = s_lo + s_hi + g_lo + g_hi;
-    char *xb = slab_xbuf(c, 48 * pay + 8 * (2 * pc + 16));
+    char *xb = slab_xbuf(c, 48 * pay + 64);
     if (!xb) return comm_fail("staging buffer allocation");
-    // scans live at the start of xbuf (rebuilt if xbuf moved: recompute)
-    if (xb != (char *)tmp) {
-        tmp = (int *)xb;
-        scan_lo = tmp;
-        scan_hi = tmp + pc;
-        if (has_lo) exclusive_scan(ArrayIn{c.count + (S.k0 - 1) * pc}, pc, scan_lo, tmp + 2 * pc, c.scan_tmp, st);
-        if (has_hi) exclusive_scan(ArrayIn{c.count + S.k1 * pc}, pc, scan_hi, tmp + 2 * pc + 1, c.scan_tmp, st);
-    }
-    double *pb = (double *)(xb + 8 * (2 * pc + 16));
+    double *pb = (double *)xb;
     double *send_lo = pb, *send_hi = send_lo + 6 * s_lo, *recv_lo = send_hi + 6 * s_hi,
            *recv_hi = recv_lo + 6 * g_lo;
     if (s_lo) k_pack_planes<<<nblocks(s_lo), kThreads, 0, st>>>(c.P, o[0], s_lo, send_lo);
@@ -537,6 +530,8 @@ extern "C" int flip_set_slab_comm(flip_ctx *ctx, int32_t rank, int32_t world,
     S.k1 = plane_start[rank + 1];
     if (!S.kstart_dev) FLIP_CUDA_OK(cudaMalloc(&S.kstart_dev, sizeof(int) * 65));
     if (!S.cnt_dev) FLIP_CUDA_OK(cudaMalloc(&S.cnt_dev, sizeof(int64_t) * 64 * 64 + 64));
+    if (!S.gscan)
+        FLIP_CUDA_OK(cudaMalloc(&S.gscan, sizeof(int) * (2 * (int64_t)c.d.nx * c.d.ny + 16)));
     std::vector<int> ks(S.kstart.begin(), S.kstart.end());
     FLIP_CUDA_OK(cudaMemcpy(S.kstart_dev, ks.data(), sizeof(int) * ks.size(), cudaMemcpyHostToDevice));
     const int64_t pc = (int64_t)c.d.nx * c.d.ny;

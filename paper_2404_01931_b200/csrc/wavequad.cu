@@ -101,20 +101,24 @@ __device__ __forceinline__ void q_cluster_tile(int t, int CB, int CC, int &bq, i
 // One cell of the substitution (k_mic_cl's arithmetic).  pv / yv / zv are
 // the contributions of the -x / -y / -z (forward) or +x / +y / +z
 // (backward) neighbours; returns the value passed on, -0.0 off the rows.
+// The lane entry is written unconditionally (no branch): the value on a
+// row, the ABSENT marker elsewhere (the next sweep's src keeps its markers;
+// rows are only ever read back through posL).
 template <bool REV>
 __device__ __forceinline__ double mic_cell(double a, double pr, double pv, double yv, double zv,
                                            double sc, bool row, double *dst) {
+    const double absent = __longlong_as_double((long long)WAVE_ABSENT);
     double o;
     if (!REV) {  // _core.pyx:322-332
         double tt = ((a + pv) + yv) + zv;
         double q = tt * pr;
-        if (row) *dst = q;
+        __stcg(dst, row ? q : absent);
         o = (sc * pr) * q;
     } else {     // _core.pyx:333-346
         double sp = sc * pr;
         double tt = ((a + sp * pv) + sp * yv) + sp * zv;
         o = tt * pr;
-        if (row) *dst = o;
+        __stcg(dst, row ? o : absent);
     }
     return row ? o : -0.0;
 }
@@ -125,8 +129,9 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
     // logical cell L (forward order (0,0), (1,0), (0,1), (1,1)) -> stored q
     // (pencil a + 2b); the backward sweep visits the block mirrored
     auto PQ = [](int L) { return REV ? 3 - L : L; };
-    // sq[buf][kk + 1][jj + 1][q]: each thread's four outputs of a step
-    __shared__ double sq[2][QT + 2][QT + 2][4];
+    // sq[buf][q][kk + 1][jj + 1]: each thread's four outputs of a step
+    // (q-planar, so a warp's loads and stores hit consecutive banks)
+    __shared__ double sq[2][4][QT + 2][QT + 2];
     __shared__ int s_tile;
     __shared__ __align__(8) unsigned long long mbar[NB];
     // yring[nsteps][QW], zring[nsteps][QW], then the operand chunks
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
     const int ry = (int)cr / CZ, rz = (int)cr % CZ;
     const double nz0 = -0.0;
     const double pend = __longlong_as_double((long long)WAVE_PENDING);
-    for (int q = t; q < 2 * (QT + 2) * (QT + 2) * 4; q += blockDim.x) (&sq[0][0][0][0])[q] = nz0;
+    for (int q = t; q < 2 * 4 * (QT + 2) * (QT + 2); q += blockDim.x) (&sq[0][0][0][0])[q] = nz0;
     for (int q = t; q < nsteps * 2 * QW; q += blockDim.x) ring[q] = pend;
     if (cr == 0 && t == 0) s_tile = atomicAdd(A.ticket, 1);
     if (t == 0) {
@@ -208,8 +213,8 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
         double hy = nz0, hz = nz0;
         if (iny) hy = DY < nsteps ? q_spin_gpu(iny + (int64_t)DY * QW) : nz0;
         if (inz) hz = DZ < nsteps ? q_spin_gpu(inz + (int64_t)DZ * QW) : nz0;
-        if (iny) sq[1][y_row][y_col][y_q] = hy;
-        if (inz) sq[1][z_row][z_col][z_q] = hz;
+        if (iny) sq[1][y_q][y_row][y_col] = hy;
+        if (inz) sq[1][z_q][z_row][z_col] = hz;
         double py = (iny && 1 + DY < nsteps) ? ld_relaxed(iny + (int64_t)(1 + DY) * QW) : nz0;
         double pz = (inz && 1 + DZ < nsteps) ? ld_relaxed(inz + (int64_t)(1 + DZ) * QW) : nz0;
         for (int s = 0; s < nsteps; s++) {
@@ -222,13 +227,13 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
             if (iny) {
                 double v = (s + 1 + DY < nsteps) ? py : nz0;
                 if (is_pending(v)) v = q_spin_gpu(iny + (int64_t)(s + 1 + DY) * QW);
-                sq[cur][y_row][y_col][y_q] = v;
+                sq[cur][y_q][y_row][y_col] = v;
                 py = (s + 2 + DY < nsteps) ? ld_relaxed(iny + (int64_t)(s + 2 + DY) * QW) : nz0;
             }
             if (inz) {
                 double v = (s + 1 + DZ < nsteps) ? pz : nz0;
                 if (is_pending(v)) v = q_spin_gpu(inz + (int64_t)(s + 1 + DZ) * QW);
-                sq[cur][z_row][z_col][z_q] = v;
+                sq[cur][z_q][z_row][z_col] = v;
                 pz = (s + 2 + DZ < nsteps) ? ld_relaxed(inz + (int64_t)(s + 2 + DZ) * QW) : nz0;
             }
         }
@@ -290,8 +295,8 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
                 // neighbour contributions from the previous step: -y feeds
                 // logical cells 0 and 2 (the -y thread's cells 1 and 3), -z
                 // feeds cells 0 and 1 (the -z thread's cells 2 and 3)
-                double y0 = sq[prv][yr][yc][PQ(1)], y2 = sq[prv][yr][yc][PQ(3)];
-                double z0 = sq[prv][zr][zc][PQ(2)], z1 = sq[prv][zr][zc][PQ(3)];
+                double y0 = sq[prv][PQ(1)][yr][yc], y2 = sq[prv][PQ(3)][yr][yc];
+                double z0 = sq[prv][PQ(2)][zr][zc], z1 = sq[prv][PQ(3)][zr][zc];
                 if (yin) {
                     if (s + DY < nsteps) {
                         y0 = q_take(ypre0, yring + (s + DY) * QW + 2 * kk);
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
                 o[3] = mic_cell<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), d + PQ(3) * QP);
 #pragma unroll
                 for (int L = 0; L < 4; L++) {
-                    sq[cur][kk + 1][jj + 1][PQ(L)] = o[L];
+                    sq[cur][PQ(L)][kk + 1][jj + 1] = o[L];
                     pv[L] = o[L];
                 }
                 if (yout) {
