@@ -1773,9 +1773,10 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     WaveGeom LG = W.geom;
     if (use_lane && mic_quad_enabled()) {
         WaveGeom qg = quad_geom(c.sch->row_lo, c.sch->row_hi);
-        const int64_t halo_need = (int64_t)qg.TB * qg.TC * qg.nsteps * 64;
+        const int64_t halo_need = (int64_t)qg.TB * qg.TC * qg.nsteps * 2 * qg.ty;
         if (lane_entries(qg) <= c.lane_cap &&
-            halo_need <= wave_halo_doubles(c.d.nx, c.d.ny, c.d.nz) - 64)
+            halo_need <= wave_halo_doubles(c.d.nx, c.d.ny, c.d.nz) - 64 &&
+            mic_quad_supported(qg.nsteps))
             LG = qg;
     }
     if (use_lane) {

@@ -835,8 +835,9 @@ __global__ void k_lane_map(WaveGeom G, Dims d, int TY, int TZ, const uint8_t *__
         int tile = (int)tq;
         int b = tile / G.TC, c = tile % G.TC;
         int i, j, k;
-        if (G.quad) {  // [q][thread]: thread (jj, kk) of 16 x 16 owns pencils (2jj + a, 2kk + b)
-            const int q = p >> 8, th = p & 255, jj = th & 15, kk = th >> 4;
+        if (G.quad) {  // [q][thread]: thread (jj, kk) of QT x QT owns pencils (2jj + a, 2kk + b)
+            const int QT = G.quad, QP = QT * QT;
+            const int q = p / QP, th = p - q * QP, kk = th / QT, jj = th - kk * QT;
             i = G.ilo + s - jj - kk;
             j = G.jlo + b * TY + 2 * jj + (q & 1);
             k = G.klo + c * TZ + 2 * kk + (q >> 1);
@@ -1118,12 +1119,13 @@ cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st) {
         const int64_t tiles = (int64_t)A.geom.TB * A.geom.TC;
         int cy = 0, cz = 0;
         quad_cluster_shape(&cy, &cz);
-        const int64_t nsel = (int64_t)(A.geom.TB / cy) * A.geom.TC * A.geom.nsteps * 32 +
-                             (int64_t)A.geom.TB * (A.geom.TC / cz) * A.geom.nsteps * 32;
+        const int QW = A.geom.ty;  // face width
+        const int64_t nsel = (int64_t)(A.geom.TB / cy) * A.geom.TC * A.geom.nsteps * QW +
+                             (int64_t)A.geom.TB * (A.geom.TC / cz) * A.geom.nsteps * QW;
         LaneArgs B = A;
-        B.halo_z = A.halo_y + tiles * A.geom.nsteps * 32;
+        B.halo_z = A.halo_y + tiles * A.geom.nsteps * QW;
         launch_pdl(k_wave_prep_cl, nblocks(nsel), kThreads, 0, st, A.halo_y, B.halo_z,
-                   A.geom.TB, A.geom.TC, A.geom.nsteps, 32, 32, cy, cz, rev ? 1 : 0, A.ticket,
+                   A.geom.TB, A.geom.TC, A.geom.nsteps, QW, QW, cy, cz, rev ? 1 : 0, A.ticket,
                    (const DevScalars *)A.sc);
         return launch_mic_quad(rev, B, st);
     }

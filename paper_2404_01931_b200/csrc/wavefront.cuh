@@ -164,6 +164,7 @@ struct LaneArgs {
 cudaError_t launch_wave(int mode, const WaveArgs &A, cudaStream_t st);
 // wavequad.cu: 2 x 2 pencils per thread (FLIPB200_QUAD=0 disables)
 bool mic_quad_enabled();
+bool mic_quad_supported(int nsteps);
 int quad_cluster_shape(int *cy, int *cz);
 WaveGeom quad_geom(const int lo[3], const int hi[3]);
 cudaError_t launch_mic_quad(bool rev, const LaneArgs &A, cudaStream_t st);

@@ -29,9 +29,6 @@ namespace flip {
 
 namespace {
 
-constexpr int QT = 16;          // threads per tile edge
-constexpr int QP = QT * QT;     // compute threads
-constexpr int QW = 2 * QT;      // face width (values per step)
 
 __device__ __forceinline__ unsigned q_smem(const void *p) { return smem_u32(p); }
 __device__ __forceinline__ unsigned q_rank() {
@@ -96,6 +93,18 @@ __device__ __forceinline__ void q_cluster_tile(int t, int CB, int CC, int &bq, i
     }
 }
 
+// Stress mode (FLIPB200_QUAD_EXP=16, tests only): pseudo-random sleeps of
+// up to ~2 us at ~1 in 8 (tile, step, thread) points perturb every
+// producer/consumer timing of the face protocol; results must not change.
+__device__ __forceinline__ void q_jitter(int X, int tile, int s, int t) {
+    if (!(X & 16)) return;
+    unsigned h = (unsigned)tile * 2654435761u ^ (unsigned)s * 40503u ^ (unsigned)t * 2246822519u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    if ((h & 7u) == 0u) __nanosleep((h >> 16) & 2047u);
+}
+
 }  // namespace
 
 // One cell of the substitution (k_mic_cl's arithmetic).  pv / yv / zv are
@@ -112,19 +121,22 @@ __device__ __forceinline__ double mic_cell(double a, double pr, double pv, doubl
     if (!REV) {  // _core.pyx:322-332
         double tt = ((a + pv) + yv) + zv;
         double q = tt * pr;
-        __stcg(dst, row ? q : absent);
+        if (dst) __stcg(dst, row ? q : absent);
         o = (sc * pr) * q;
     } else {     // _core.pyx:333-346
         double sp = sc * pr;
         double tt = ((a + sp * pv) + sp * yv) + sp * zv;
         o = tt * pr;
-        __stcg(dst, row ? o : absent);
+        if (dst) __stcg(dst, row ? o : absent);
     }
     return row ? o : -0.0;
 }
 
-template <bool REV, int CY, int CZ, int KC, int NB>
-__global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
+// QT threads per tile edge (16 or 8): a tile is 2QT x 2QT pencils, the
+// faces are QW = 2QT values wide.
+template <bool REV, int QT, int CY, int CZ, int KC, int NB>
+__global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
+    constexpr int QP = QT * QT, QW = 2 * QT;
     constexpr int DY = QT - 1, DZ = QT - 1;
     // logical cell L (forward order (0,0), (1,0), (0,1), (1,1)) -> stored q
     // (pencil a + 2b); the backward sweep visits the block mirrored
@@ -163,6 +175,13 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
         c = G.TC - 1 - c;
     }
     const int tile = b * G.TC + c;
+    unsigned long long *trace = (!REV && A.trace) ? A.trace : nullptr;  // FLIPB200_WAVE_TRACE
+    if (trace && t == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        trace[4 * tile + 0] = g;
+        trace[4 * tile + 3] = (unsigned long long)b << 16 | (unsigned)c;
+    }
     auto lstep = [&](int s) { return REV ? nsteps - 1 - s : s; };
     const bool ydin = ry > 0, ydout = ry < CY - 1;
     const bool zdin = rz > 0, zdout = rz < CZ - 1;
@@ -190,51 +209,65 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
         // logical cell 0, e = 1 cell 2) and z-face word l (consumer jj =
         // l/2; e = 0 feeds cell 0, e = 1 cell 1)
         const int l = t - QP;
+        // y word ly and z word lz of this lane (-1: none)
+        const int ly = QW == 32 ? l : (l < QW ? l : -1);
+        const int lz = QW == 32 ? l : (l >= 32 - QW ? l - (32 - QW) : -1);
+        // The helper also forwards the faces that arrive by DSMEM (from its
+        // own rings), so no compute lane polls or diverges on face code
+        // (measured: 176.4 -> 169.2 us per sweep at 256^3).
+        const bool HF = true;
         const double *iny = nullptr, *inz = nullptr;
+        const double *ly_ring = nullptr, *lz_ring = nullptr;
         {
             const bool has = REV ? b + 1 < G.TB : b > 0;
-            if (has && !ydin)
-                iny = A.halo_y + (int64_t)(REV ? tile + G.TC : tile - G.TC) * nsteps * QW + l;
+            if (has && !ydin && ly >= 0)
+                iny = A.halo_y + (int64_t)(REV ? tile + G.TC : tile - G.TC) * nsteps * QW + ly;
+            if (HF && ydin && ly >= 0) ly_ring = yring + ly;
             const bool hasz = REV ? c + 1 < G.TC : c > 0;
-            if (hasz && !zdin)
-                inz = A.halo_z + (int64_t)(REV ? tile + 1 : tile - 1) * nsteps * QW + l;
+            if (hasz && !zdin && lz >= 0)
+                inz = A.halo_z + (int64_t)(REV ? tile + 1 : tile - 1) * nsteps * QW + lz;
+            if (HF && zdin && lz >= 0) lz_ring = zring + lz;
         }
         // where the value lands: the consumer reads its -y (-z) neighbour
         // thread's stored output of the producing logical cell
-        const int e = l & 1, h = l >> 1;
-        const int y_row = h + 1, y_col = REV ? QT + 1 : 0, y_q = PQ(e == 0 ? 1 : 3);
-        const int z_row = REV ? QT + 1 : 0, z_col = h + 1, z_q = PQ(e == 0 ? 2 : 3);
+        const int ey = ly & 1, hy_ = ly >> 1, ez = lz & 1, hz_ = lz >> 1;
+        const int y_row = hy_ + 1, y_col = REV ? QT + 1 : 0, y_q = PQ(ey == 0 ? 1 : 3);
+        const int z_row = REV ? QT + 1 : 0, z_col = hz_ + 1, z_q = PQ(ez == 0 ? 2 : 3);
         // the consumer lanes must lie in the rows' box
         const int cons_j = REV ? QT - 1 : 0, cons_k = REV ? QT - 1 : 0;
-        if (!(G.jlo + b * QW + 2 * cons_j <= G.jhi && G.klo + c * QW + 2 * h <= G.khi)) iny = nullptr;
-        if (!(G.jlo + b * QW + 2 * h <= G.jhi && G.klo + c * QW + 2 * cons_k <= G.khi)) inz = nullptr;
+        if (!(G.jlo + b * QW + 2 * cons_j <= G.jhi && G.klo + c * QW + 2 * hy_ <= G.khi)) iny = ly_ring = nullptr;
+        if (!(G.jlo + b * QW + 2 * hz_ <= G.jhi && G.klo + c * QW + 2 * cons_k <= G.khi)) inz = lz_ring = nullptr;
         if (l == 0)
             for (int q = 0; q < NB; q++) issue(q);
-        double hy = nz0, hz = nz0;
-        if (iny) hy = DY < nsteps ? q_spin_gpu(iny + (int64_t)DY * QW) : nz0;
-        if (inz) hz = DZ < nsteps ? q_spin_gpu(inz + (int64_t)DZ * QW) : nz0;
-        if (iny) sq[1][y_q][y_row][y_col] = hy;
-        if (inz) sq[1][z_q][z_row][z_col] = hz;
-        double py = (iny && 1 + DY < nsteps) ? ld_relaxed(iny + (int64_t)(1 + DY) * QW) : nz0;
-        double pz = (inz && 1 + DZ < nsteps) ? ld_relaxed(inz + (int64_t)(1 + DZ) * QW) : nz0;
+        // slot of producer step sp: global halo or local DSMEM ring
+        auto peek_y = [&](int sp) { return iny ? ld_relaxed(iny + (int64_t)sp * QW) : q_peek(ly_ring + sp * QW); };
+        auto spin_y = [&](int sp) { return iny ? q_spin_gpu(iny + (int64_t)sp * QW) : q_poll(ly_ring + sp * QW); };
+        auto peek_z = [&](int sp) { return inz ? ld_relaxed(inz + (int64_t)sp * QW) : q_peek(lz_ring + sp * QW); };
+        auto spin_z = [&](int sp) { return inz ? q_spin_gpu(inz + (int64_t)sp * QW) : q_poll(lz_ring + sp * QW); };
+        const bool fy = iny || ly_ring, fz = inz || lz_ring;
+        if (fy) sq[1][y_q][y_row][y_col] = DY < nsteps ? spin_y(DY) : nz0;
+        if (fz) sq[1][z_q][z_row][z_col] = DZ < nsteps ? spin_z(DZ) : nz0;
+        double py = (fy && 1 + DY < nsteps) ? peek_y(1 + DY) : nz0;
+        double pz = (fz && 1 + DZ < nsteps) ? peek_z(1 + DZ) : nz0;
         for (int s = 0; s < nsteps; s++) {
             __syncthreads();
-            if (l == 0 && s > 0 && s % KC == 0) {
+            if (l == 0 && s > 0 && s % KC == 0 && !(A.dbg & 1)) {
                 fence_proxy_async();
                 issue(s / KC - 1 + NB);
             }
             const int cur = s & 1;
-            if (iny) {
+            q_jitter(A.dbg, tile, s, t);
+            if (fy) {
                 double v = (s + 1 + DY < nsteps) ? py : nz0;
-                if (is_pending(v)) v = q_spin_gpu(iny + (int64_t)(s + 1 + DY) * QW);
+                if (is_pending(v)) v = spin_y(s + 1 + DY);
                 sq[cur][y_q][y_row][y_col] = v;
-                py = (s + 2 + DY < nsteps) ? ld_relaxed(iny + (int64_t)(s + 2 + DY) * QW) : nz0;
+                py = (s + 2 + DY < nsteps) ? peek_y(s + 2 + DY) : nz0;
             }
-            if (inz) {
+            if (fz) {
                 double v = (s + 1 + DZ < nsteps) ? pz : nz0;
-                if (is_pending(v)) v = q_spin_gpu(inz + (int64_t)(s + 1 + DZ) * QW);
+                if (is_pending(v)) v = spin_z(s + 1 + DZ);
                 sq[cur][z_q][z_row][z_col] = v;
-                pz = (s + 2 + DZ < nsteps) ? ld_relaxed(inz + (int64_t)(s + 2 + DZ) * QW) : nz0;
+                pz = (s + 2 + DZ < nsteps) ? peek_z(s + 2 + DZ) : nz0;
             }
         }
         __syncthreads();
@@ -251,8 +284,6 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
         }
         const int cons_j = REV ? QT - 1 : 0, cons_k = REV ? QT - 1 : 0;
         const int prod_j = REV ? 0 : QT - 1, prod_k = REV ? 0 : QT - 1;
-        const bool yin = ydin && jj == cons_j;
-        const bool zin = zdin && kk == cons_k;
         // producing lanes: DSMEM into the next CTA of the cluster, or the
         // global halo when the face leaves the cluster
         const unsigned yout = (ydout && jj == prod_j) ? q_map(yring + 2 * kk, cr + CZ) : 0u;
@@ -262,21 +293,13 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
         const int64_t base = (int64_t)tile * nsteps * TS + t;
         double *dstL = A.dst + base;
         double pv[4] = {nz0, nz0, nz0, nz0};
-        double ypre0 = pend, ypre1 = pend, zpre0 = pend, zpre1 = pend;
-        if (yin && DY < nsteps) {
-            ypre0 = q_peek(yring + DY * QW + 2 * kk);
-            ypre1 = q_peek(yring + DY * QW + 2 * kk + 1);
-        }
-        if (zin && DZ < nsteps) {
-            zpre0 = q_peek(zring + DZ * QW + 2 * jj);
-            zpre1 = q_peek(zring + DZ * QW + 2 * jj + 1);
-        }
         const double sc = A.scale;
         const int yr = kk + 1, yc = jj + nbo, zr = kk + nbo, zc = jj + 1;
+        const int X = A.dbg;  // timing experiments only (FLIPB200_QUAD_EXP): results differ
         for (int ch = 0; ch < nch; ch++) {
             const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
             const int buf = ch % NB;
-            mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
+            if (!(X & 1) || ch < NB) mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
             const double *ab = opb + (buf * 2 + 0) * KC * TS + t;
             const double *pb = opb + (buf * 2 + 1) * KC * TS + t;
 #pragma unroll
@@ -284,6 +307,12 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
                 if (u >= cnt) break;
                 const int s = s0 + u;
                 __syncthreads();
+                if (trace && t == 0 && (s == 0 || (tile < 8 && s < 300))) {
+                    unsigned long long g;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+                    if (tile < 8 && s < 300) trace[20000 + tile * 300 + s] = g;
+                    if (s == 0) trace[4 * tile + 2] = g;
+                }
                 const int cur = s & 1, prv = cur ^ 1;
                 const int idx = REV ? cnt - 1 - u : u;
                 double a[4], pr[4];
@@ -297,41 +326,27 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
                 // feeds cells 0 and 1 (the -z thread's cells 2 and 3)
                 double y0 = sq[prv][PQ(1)][yr][yc], y2 = sq[prv][PQ(3)][yr][yc];
                 double z0 = sq[prv][PQ(2)][zr][zc], z1 = sq[prv][PQ(3)][zr][zc];
-                if (yin) {
-                    if (s + DY < nsteps) {
-                        y0 = q_take(ypre0, yring + (s + DY) * QW + 2 * kk);
-                        y2 = q_take(ypre1, yring + (s + DY) * QW + 2 * kk + 1);
-                    } else {
-                        y0 = y2 = nz0;
-                    }
-                    if (s + 1 + DY < nsteps) {
-                        ypre0 = q_peek(yring + (s + 1 + DY) * QW + 2 * kk);
-                        ypre1 = q_peek(yring + (s + 1 + DY) * QW + 2 * kk + 1);
-                    }
-                }
-                if (zin) {
-                    if (s + DZ < nsteps) {
-                        z0 = q_take(zpre0, zring + (s + DZ) * QW + 2 * jj);
-                        z1 = q_take(zpre1, zring + (s + DZ) * QW + 2 * jj + 1);
-                    } else {
-                        z0 = z1 = nz0;
-                    }
-                    if (s + 1 + DZ < nsteps) {
-                        zpre0 = q_peek(zring + (s + 1 + DZ) * QW + 2 * jj);
-                        zpre1 = q_peek(zring + (s + 1 + DZ) * QW + 2 * jj + 1);
-                    }
-                }
                 double *d = dstL + (int64_t)lstep(s) * TS;
+                const bool nost = X & 2;
                 double o[4];
-                o[0] = mic_cell<REV>(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), d + PQ(0) * QP);
-                o[1] = mic_cell<REV>(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), d + PQ(1) * QP);
-                o[2] = mic_cell<REV>(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), d + PQ(2) * QP);
-                o[3] = mic_cell<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), d + PQ(3) * QP);
+                if (X & 4) {
+#pragma unroll
+                    for (int L = 0; L < 4; L++) o[L] = a[L] + pr[L];
+                    o[0] = o[0] + y0 + z0;
+                    o[1] = o[1] + z1;
+                    o[2] = o[2] + y2;
+                } else {
+                o[0] = mic_cell<REV>(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), nost ? nullptr : d + PQ(0) * QP);
+                o[1] = mic_cell<REV>(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), nost ? nullptr : d + PQ(1) * QP);
+                o[2] = mic_cell<REV>(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), nost ? nullptr : d + PQ(2) * QP);
+                o[3] = mic_cell<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), nost ? nullptr : d + PQ(3) * QP);
+                }
 #pragma unroll
                 for (int L = 0; L < 4; L++) {
                     sq[cur][PQ(L)][kk + 1][jj + 1] = o[L];
                     pv[L] = o[L];
                 }
+                q_jitter(X, tile, s, t);
                 if (yout) {
                     q_st_remote(yout + (unsigned)(s * QW * 8), o[1]);
                     q_st_remote(yout + (unsigned)(s * QW * 8 + 8), o[3]);
@@ -351,15 +366,22 @@ __global__ void __launch_bounds__(QP + 32) k_mic_quad(LaneArgs A) {
             }
         }
         __syncthreads();  // matches the helper's final barrier
+        if (trace && t == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+            trace[4 * tile + 1] = g;
+        }
     }
     q_cluster_sync();  // no CTA leaves while a peer can still store into its rings
 }
 
 // ------------------------------------------------------------- launching --
+int quad_threads();
+
 int quad_cluster_shape(int *cy, int *cz) {
     static int y = -1, z = -1;
     if (y < 0) {
-        y = 2;
+        y = quad_threads() == 16 ? 2 : 4;
         z = 4;
         if (const char *e = getenv("FLIPB200_QUAD_CLUSTER")) {
             int a = 0, b = 0;
@@ -382,11 +404,21 @@ bool mic_quad_enabled() {
     return on != 0;
 }
 
-// Quad geometry: tiles of 32 x 32 pencils, 16 x 16 threads, padded to whole
-// clusters; nsteps = ispan + 2 * (16 - 1).
+int quad_threads() {  // threads per tile edge (FLIPB200_QUAD_QT: 16 or 8)
+    static const int q = [] {
+        const char *e = getenv("FLIPB200_QUAD_QT");
+        const int v = e ? atoi(e) : 8;
+        return v == 16 ? 16 : 8;
+    }();
+    return q;
+}
+
+// Quad geometry: tiles of 2QT x 2QT pencils, QT x QT threads, padded to
+// whole clusters; nsteps = ispan + 2 * (QT - 1).
 WaveGeom quad_geom(const int lo[3], const int hi[3]) {
     int cy, cz;
     quad_cluster_shape(&cy, &cz);
+    const int QT = quad_threads(), QW = 2 * QT;
     WaveGeom g{};
     g.ilo = lo[0];
     g.ihi = hi[0];
@@ -403,21 +435,22 @@ WaveGeom quad_geom(const int lo[3], const int hi[3]) {
     g.ispan = hi[0] - lo[0] + 1;
     g.ispan_pad = (g.ispan + 1) & ~1;
     g.nsteps = g.ispan + 2 * (QT - 1);
-    g.quad = 1;
+    g.quad = QT;
     return g;
 }
 
-template <bool REV, int CY, int CZ, int KC, int NB>
+template <bool REV, int QT, int CY, int CZ, int KC, int NB>
 static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
+    constexpr int QP = QT * QT, QW = 2 * QT;
     const int tiles = A.geom.TB * A.geom.TC;
     const size_t rings = ((size_t)A.geom.nsteps * 2 * QW * sizeof(double) + 127) / 128 * 128;
     const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double);
     static cudaError_t attr = [] {
-        cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, CY, CZ, KC, NB>,
+        cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024 - 24 * 1024);
         if (e == cudaSuccess && CY * CZ > 8)
-            e = cudaFuncSetAttribute(k_mic_quad<REV, CY, CZ, KC, NB>,
+            e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         return e;
     }();
@@ -437,14 +470,45 @@ static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_quad<REV, CY, CZ, KC, NB>, A);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_quad<REV, QT, CY, CZ, KC, NB>, A);
     return e != cudaSuccess ? e : cudaPeekAtLastError();
+}
+
+// Can the configured quad kernel's clusters be scheduled on this device
+// (16-CTA clusters are non-portable)?  Checked once per process.
+template <int QT, int CY, int CZ, int KC, int NB>
+static bool quad_fits(int nsteps) {
+    constexpr int QP = QT * QT, QW = 2 * QT;
+    const size_t rings = ((size_t)nsteps * 2 * QW * sizeof(double) + 127) / 128 * 128;
+    const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double);
+    auto k = k_mic_quad<false, QT, CY, CZ, KC, NB>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024 - 24 * 1024) != cudaSuccess)
+        return false;
+    if (CY * CZ > 8 &&
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CY * CZ);
+    cfg.blockDim = dim3(QP + 32);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CY * CZ;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const bool ok = cudaOccupancyMaxActiveClusters(&n, k, &cfg) == cudaSuccess && n > 0;
+    cudaGetLastError();
+    return ok;
 }
 
 static int quad_chunks() {
     static int v = -1;
     if (v < 0) {
-        int a = 2, b = 3;
+        int a = 0, b = 0;
         if (const char *e = getenv("FLIPB200_QUAD_CHUNKS")) sscanf(e, "%dx%d", &a, &b);
         v = a * 100 + b;
     }
@@ -453,16 +517,25 @@ static int quad_chunks() {
 
 template <bool REV, int CY, int CZ>
 static cudaError_t launch_quad_c(const LaneArgs &A, cudaStream_t st) {
-    switch (quad_chunks()) {
-        case 202: return launch_quad_k<REV, CY, CZ, 2, 2>(A, st);
-        case 204: return launch_quad_k<REV, CY, CZ, 2, 4>(A, st);
-        case 402: return launch_quad_k<REV, CY, CZ, 4, 2>(A, st);
-        case 103: return launch_quad_k<REV, CY, CZ, 1, 3>(A, st);
-        default: return launch_quad_k<REV, CY, CZ, 2, 3>(A, st);
+    if (A.geom.quad == 16) {
+        switch (quad_chunks()) {
+            case 204: return launch_quad_k<REV, 16, CY, CZ, 2, 4>(A, st);
+            default: return launch_quad_k<REV, 16, CY, CZ, 2, 3>(A, st);
+        }
+    }
+    switch (quad_chunks()) {  // QT = 8: 2 KB of operands per array and step
+        case 403: return launch_quad_k<REV, 8, CY, CZ, 4, 3>(A, st);
+        case 404: return launch_quad_k<REV, 8, CY, CZ, 4, 4>(A, st);
+        case 803: return launch_quad_k<REV, 8, CY, CZ, 8, 3>(A, st);
+        case 1602: return launch_quad_k<REV, 8, CY, CZ, 16, 2>(A, st);
+        default: return launch_quad_k<REV, 8, CY, CZ, 8, 2>(A, st);
     }
 }
 
-cudaError_t launch_mic_quad(bool rev, const LaneArgs &A, cudaStream_t st) {
+cudaError_t launch_mic_quad(bool rev, const LaneArgs &A0, cudaStream_t st) {
+    static const int exp_flags = getenv("FLIPB200_QUAD_EXP") ? atoi(getenv("FLIPB200_QUAD_EXP")) : 0;
+    LaneArgs A = A0;
+    A.dbg = exp_flags;
     int cy, cz;
     quad_cluster_shape(&cy, &cz);
     if (!A.geom.quad || A.geom.TB % cy || A.geom.TC % cz) return cudaErrorNotSupported;
@@ -474,8 +547,21 @@ cudaError_t launch_mic_quad(bool rev, const LaneArgs &A, cudaStream_t st) {
     QCASE(4, 2)
     QCASE(1, 4)
     QCASE(1, 1)
+    QCASE(2, 8)
+    QCASE(4, 8)
 #undef QCASE
     return cudaErrorNotSupported;
+}
+
+bool mic_quad_supported(int nsteps) {
+    int cy, cz;
+    quad_cluster_shape(&cy, &cz);
+    const int key = cy * 100 + cz;
+    // the default shape / chunking of each tile edge (what launch_quad_c picks)
+    if (quad_threads() == 8 && key == 404 && (quad_chunks() == 0 || quad_chunks() == 802))
+        return quad_fits<8, 4, 4, 8, 2>(nsteps);
+    if (quad_threads() == 16 && key == 204) return quad_fits<16, 2, 4, 2, 3>(nsteps);
+    return cy * cz <= 16;  // other (experimental) shapes: the launch reports misfits
 }
 
 }  // namespace flip

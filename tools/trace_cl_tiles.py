@@ -11,7 +11,10 @@ RES = int(os.environ.get("RES", "256"))
 spec = P.SceneSpec(name="dam-break", res=RES, max_iters=1)
 st = P.make_scene(spec, 0)
 for _ in range(int(os.environ.get("STEPS", "8"))):
-    P.step(st, spec)
+    try:
+        P.step(st, spec)
+    except P.SolverError:  # timing experiments (FLIPB200_QUAD_EXP) break the numerics
+        pass
 tr = st.device.debug_buffer("wave_trace", 32768, dtype=np.uint64).astype(np.int64)
 t4 = tr[:4 * 4096].reshape(-1, 4)
 m = t4[:, 1] > 0
