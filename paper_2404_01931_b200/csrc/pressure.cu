@@ -1217,9 +1217,10 @@ __global__ void __launch_bounds__(256)
 k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
              const double *__restrict__ s, const double *__restrict__ q, DevScalars *sc,
              double *__restrict__ rL, const int *__restrict__ posL, int64_t max_iters,
-             double *history, int check) {
+             double *history, int check, HaloReset H) {
     pdl_wait();
     if (sc->done) return;
+    halo_reset(H, gtid(), gstride());  // the next two MIC(0) sweeps' halo slots
     __shared__ double wm[8];
     __shared__ bool last;
     const double alpha = sc->alpha;
@@ -1269,6 +1270,64 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
                 (long long)atomicAdd(&sc->res_bits, 0ull));
             // slab mode (check 0): the test runs after the MAX allreduce
             if (check) iter_check_body(sc, max_iters, history, res);
+        }
+    }
+}
+
+// k_pcg_update walked in LANE order (one GPU, MIC(0) lane path): thread =
+// one lane of the sweep layout for kLaneRun consecutive steps, i.e. one
+// x-run of consecutive rows.  The r -> L scatter of the row-order kernel
+// (one 32-byte sector per 8-byte store) becomes coalesced stores across the
+// warp, and the row-order loads/stores of a thread hit one sector per
+// kLaneRun rows.  Same per-row arithmetic; max|r| is order-free.
+constexpr int kLaneRun = 4;
+__global__ void __launch_bounds__(256)
+k_pcg_update_lane(const int *__restrict__ lrow, int64_t ntiles, int nsteps, int TS,
+                  double *__restrict__ x, double *__restrict__ r, const double *__restrict__ s,
+                  const double *__restrict__ q, DevScalars *sc, double *__restrict__ rL,
+                  int64_t max_iters, double *history, HaloReset H) {
+    pdl_wait();
+    if (sc->done) return;
+    halo_reset(H, gtid(), gstride());
+    __shared__ double wm[8];
+    __shared__ bool last;
+    const double alpha = sc->alpha;
+    const int nchunk = (nsteps + kLaneRun - 1) / kLaneRun;
+    const int64_t items = ntiles * nchunk * TS;
+    double m = 0.0;
+    for (int64_t w = gtid(); w < items; w += gstride()) {
+        const int64_t p = w % TS, tc = w / TS;
+        const int64_t tile = tc / nchunk;
+        const int s0 = (int)(tc - tile * nchunk) * kLaneRun;
+        const int64_t e0 = (tile * nsteps + s0) * TS + p;
+        int rows[kLaneRun];
+#pragma unroll
+        for (int u = 0; u < kLaneRun; u++)
+            rows[u] = s0 + u < nsteps ? __ldg(lrow + e0 + (int64_t)u * TS) : -1;
+#pragma unroll
+        for (int u = 0; u < kLaneRun; u++) {
+            const int i = rows[u];
+            if (i < 0) continue;
+            x[i] = x[i] + alpha * s[i];
+            const double ri = r[i] - alpha * q[i];
+            r[i] = ri;
+            rL[e0 + (int64_t)u * TS] = ri;
+            m = fmax(m, fabs(ri));
+        }
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmax(m, wm[w]);
+        if (m > 0.0) atomic_max_nonneg(&sc->res_bits, m);
+        __threadfence();
+        last = atomicAdd(&sc->upd_ticket, 1u) == gridDim.x - 1;
+        if (last) {
+            sc->upd_ticket = 0u;
+            const double res = __longlong_as_double(
+                (long long)atomicAdd(&sc->res_bits, 0ull));
+            iter_check_body(sc, max_iters, history, res);
         }
     }
 }
@@ -1354,6 +1413,8 @@ struct LaneBufs {
     LaneArgs args;       // geometry, halos, ticket, scale
     const int *posL;     // row -> L entry
     double *rL, *tqL, *zL, *preL;
+    const int *lrow = nullptr;  // L entry -> row (-1: none), k_lane_map
+    HaloReset hr{};      // quad: per-direction halo buffers, reset by k_pcg_update
 };
 
 struct SweepLevels {
@@ -1410,6 +1471,25 @@ static void do_sweep(const SysView &S, const SweepLevels &LV, const double *src,
 // caller's k_pcg_update and z.r dot (r already in Lb.rL, z left in Lb.zL).
 // (Scattering z into row order from inside the backward sweep instead was
 // measured slower: +36 us per sweep for -21 us in the dot at 256^3.)
+// Pinned read-back slots of the solver's done flag (one ring per host
+// thread and device; see run_solve).
+constexpr int kPollDepth = 3;
+struct PollRing {
+    DevScalars *h = nullptr;
+    cudaEvent_t ev[kPollDepth] = {};
+};
+static PollRing &poll_ring() {
+    static thread_local PollRing rings[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    PollRing &r = rings[dev & 63];
+    if (!r.h) {
+        cudaMallocHost((void **)&r.h, sizeof(DevScalars) * kPollDepth);
+        for (auto &e : r.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    return r;
+}
+
 // Comm failure inside the solve loop (slab mode): the first one fails it.
 static thread_local int g_slab_err = 0;
 
@@ -1465,6 +1545,11 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             A.dst = rev ? Lb.zL : Lb.tqL;
             A.precon = Lb.preL;
             A.sc = sc;
+            if (Lb.hr.on) {  // quad: own halo buffer and ticket per direction
+                A.halo_y = Lb.hr.hy[rev];
+                A.ticket = Lb.hr.ticket[rev];
+                A.prepped = fused ? 1 : 0;  // in the loop k_pcg_update reset them
+            }
             bool probed = pb && pb->kind == 1 && pb->used < Probe::kMax;
             if (probed) cudaEventRecord(pb->ev[2 * pb->used], st);
             cudaError_t e = launch_mic_lane(rev != 0, A, st);
@@ -1527,7 +1612,8 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
         k_fill<<<nblocks(nf), kThreads, 0, st>>>(B.x, nf, 0.0);
         (*launches)++;
     }
-    int every = cfg.check_every > 0 ? cfg.check_every : (relax ? 64 : 8);
+    static const int every_env = getenv("FLIPB200_CHECK_EVERY") ? atoi(getenv("FLIPB200_CHECK_EVERY")) : 0;
+    int every = cfg.check_every > 0 ? cfg.check_every : every_env > 0 ? every_env : (relax ? 64 : 8);
     const bool lane = cfg.precond == FLIP_PRECOND_MIC0 && LV.lane;
     if (nf > 0 && !relax) {
         if (cfg.precond == FLIP_PRECOND_MIC0) {
@@ -1553,7 +1639,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
         // gathered rhs (every rank then holds the same full iterate)
         slab_gather_rows(cfg, const_cast<double *>(S.rhs));
     }
-    int64_t it = 0;
+    int64_t it = 0, nbatch = 0, seen = 0;
     while (nf > 0 && it < cfg.max_iters) {
         int64_t batch = std::min<int64_t>(every, cfg.max_iters - it);
         for (int64_t b = 0; b < batch; b++) {
@@ -1575,11 +1661,26 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                     solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
                     (*launches)++;
                 }
-                launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n, B.x + o,
-                           B.r + o, (const double *)(B.s + o), (const double *)(B.q + o), sc,
-                           (lane && !sl) ? LV.lane->rL : nullptr,
-                           (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
-                           (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1);
+                static const bool row_update = getenv("FLIPB200_ROW_UPDATE") != nullptr;
+                if (lane && !sl && LV.lane->lrow && !row_update) {
+                    const LaneBufs &Lb = *LV.lane;
+                    const WaveGeom &G = Lb.args.geom;
+                    const int TS = G.ty * G.tz;
+                    const int64_t items = (int64_t)G.TB * G.TC *
+                                          ((G.nsteps + kLaneRun - 1) / kLaneRun) * TS;
+                    launch_pdl(k_pcg_update_lane, wave_blocks(k_pcg_update_lane, items), kThreads,
+                               0, st, (const int *)Lb.lrow, (int64_t)G.TB * G.TC, G.nsteps, TS,
+                               B.x, B.r, (const double *)B.s, (const double *)B.q, sc, Lb.rL,
+                               (int64_t)cfg.max_iters, cfg.history, Lb.hr);
+                } else {
+                    launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
+                               B.x + o, B.r + o, (const double *)(B.s + o),
+                               (const double *)(B.q + o), sc,
+                               (lane && !sl) ? LV.lane->rL : nullptr,
+                               (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
+                               (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1,
+                               lane ? LV.lane->hr : HaloReset{});
+                }
                 if (sl) {
                     slab_max(cfg, &sc->res_bits);
                     k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
@@ -1640,10 +1741,34 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             }
         }
         it += batch;
-        cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
-        FLIP_CUDA_OK(cudaStreamSynchronize(st));
-        if (g_slab_err) return g_slab_err;
-        if (sch->done) break;
+        if (sl) {  // every rank polls after the same batch (the batches hold collectives)
+            cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
+            FLIP_CUDA_OK(cudaStreamSynchronize(st));
+            if (g_slab_err) return g_slab_err;
+            if (sch->done) break;
+            continue;
+        }
+        // one GPU: the done flag is read back asynchronously (pinned slot +
+        // event per batch), so the stream never drains at a poll; at most
+        // kPollDepth batches are in flight past the newest flag seen (after
+        // convergence their kernels exit at once on the device flag)
+        PollRing &pr = poll_ring();
+        const int slot = (int)(nbatch % kPollDepth);
+        cudaMemcpyAsync(&pr.h[slot], sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
+        cudaEventRecord(pr.ev[slot], st);
+        nbatch++;
+        bool stop = false;
+        while (seen < nbatch) {
+            const int q = (int)(seen % kPollDepth);
+            if (nbatch - seen < kPollDepth && cudaEventQuery(pr.ev[q]) == cudaErrorNotReady) break;
+            FLIP_CUDA_OK(cudaEventSynchronize(pr.ev[q]));
+            seen++;
+            if (pr.h[q].done) {
+                stop = true;
+                break;
+            }
+        }
+        if (stop) break;
     }
     if (sl && nf > 0 && !relax) slab_halo(cfg, B.x);  // pressure_field reads planes k0-1, k1
     if (g_slab_err) return g_slab_err;
@@ -1788,7 +1913,17 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         LB.args.trace = getenv("FLIPB200_WAVE_TRACE") ? c.wave_trace : nullptr;
         if (LB.args.trace) cudaMemsetAsync(c.wave_trace, 0, 8 * 32768, st);  // (trace buffer: 32768 u64)
         LB.args.dbg = getenv("FLIPB200_LANE_DBG") ? atoi(getenv("FLIPB200_LANE_DBG")) : 0;
+        if (LG.quad) {
+            int cy = 0, cz = 0;
+            quad_cluster_shape(&cy, &cz);
+            const int64_t per = (int64_t)LG.TB * LG.TC * LG.nsteps * 2 * LG.ty;
+            if (2 * per + 64 <= wave_halo_doubles(c.d.nx, c.d.ny, c.d.nz)) {
+                LB.hr = HaloReset{{c.wave_halo, c.wave_halo + per}, {c.wave_prog, c.wave_prog + 1},
+                                  LG.TB, LG.TC, LG.nsteps, LG.ty, cy, cz, 1};
+            }
+        }
         LB.posL = c.posL;
+        LB.lrow = c.lrow;
         LB.rL = c.laneA;
         LB.tqL = c.laneB;
         LB.zL = c.laneC;

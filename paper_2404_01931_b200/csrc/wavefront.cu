@@ -1124,7 +1124,7 @@ cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st) {
                              (int64_t)A.geom.TB * (A.geom.TC / cz) * A.geom.nsteps * QW;
         LaneArgs B = A;
         B.halo_z = A.halo_y + tiles * A.geom.nsteps * QW;
-        launch_pdl(k_wave_prep_cl, nblocks(nsel), kThreads, 0, st, A.halo_y, B.halo_z,
+        if (!A.prepped) launch_pdl(k_wave_prep_cl, nblocks(nsel), kThreads, 0, st, A.halo_y, B.halo_z,
                    A.geom.TB, A.geom.TC, A.geom.nsteps, QW, QW, cy, cz, rev ? 1 : 0, A.ticket,
                    (const DevScalars *)A.sc);
         return launch_mic_quad(rev, B, st);

@@ -159,7 +159,48 @@ struct LaneArgs {
     const DevScalars *sc;
     unsigned long long *trace;  // optional per-step clock of tile 0 lane 0
     int dbg;                    // traced tile index (FLIPB200_LANE_DBG, with FLIPB200_WAVE_TRACE)
+    int prepped = 0;            // quad: halo + ticket already reset (by k_pcg_update)
 };
+
+// Reset of the quad sweeps' cross-cluster halo slots and tickets, folded
+// into the kernel that precedes the forward sweep (k_pcg_update) instead of
+// one k_wave_prep_cl launch per sweep.  Buffer 0 serves the forward sweep,
+// buffer 1 the backward one (k_wave_prep_cl's slot selection with rev 0/1).
+struct HaloReset {
+    double *hy[2];
+    int *ticket[2];
+    int TB, TC, nsteps, W, cy, cz;
+    int on;
+};
+__device__ __forceinline__ void halo_reset(const HaloReset &H, int64_t tid, int64_t stride) {
+    if (!H.on) return;
+    if (tid == 0) {
+        *H.ticket[0] = 0;
+        *H.ticket[1] = 0;
+    }
+    const double m = __longlong_as_double((long long)WAVE_PENDING);
+    const int64_t tiles = (int64_t)H.TB * H.TC;
+    const int64_t yrow = (int64_t)H.TC * H.nsteps * H.W;
+    const int64_t ny = (int64_t)(H.TB / H.cy) * yrow;
+    const int64_t ztile = (int64_t)H.nsteps * H.W;
+    const int64_t nzs = (int64_t)H.TB * (H.TC / H.cz) * ztile;
+    for (int64_t e = tid; e < 2 * (ny + nzs); e += stride) {
+        const int rev = e >= ny + nzs;
+        const int64_t f0 = rev ? e - (ny + nzs) : e;
+        double *hy = rev ? H.hy[1] : H.hy[0];
+        double *hz = hy + tiles * H.nsteps * H.W;
+        if (f0 < ny) {
+            const int64_t q = f0 / yrow;
+            const int64_t b = rev ? q * H.cy : q * H.cy + H.cy - 1;
+            hy[b * yrow + f0 % yrow] = m;
+        } else {
+            const int64_t f = f0 - ny, t = f / ztile;
+            const int64_t b = t / (H.TC / H.cz), qc = t % (H.TC / H.cz);
+            const int64_t c = rev ? qc * H.cz : qc * H.cz + H.cz - 1;
+            hz[(b * H.TC + c) * ztile + f % ztile] = m;
+        }
+    }
+}
 
 cudaError_t launch_wave(int mode, const WaveArgs &A, cudaStream_t st);
 // wavequad.cu: 2 x 2 pencils per thread (FLIPB200_QUAD=0 disables)

@@ -7,6 +7,8 @@ import time
 
 import torch
 
+import os as _o, sys as _s
+_s.path.insert(0, _o.path.dirname(_o.path.dirname(_o.path.abspath(__file__))))
 import paper_2404_01931_b200 as P
 
 res = int(sys.argv[1]) if len(sys.argv) > 1 else 256
