@@ -1274,64 +1274,6 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
     }
 }
 
-// k_pcg_update walked in LANE order (one GPU, MIC(0) lane path): thread =
-// one lane of the sweep layout for kLaneRun consecutive steps, i.e. one
-// x-run of consecutive rows.  The r -> L scatter of the row-order kernel
-// (one 32-byte sector per 8-byte store) becomes coalesced stores across the
-// warp, and the row-order loads/stores of a thread hit one sector per
-// kLaneRun rows.  Same per-row arithmetic; max|r| is order-free.
-constexpr int kLaneRun = 4;
-__global__ void __launch_bounds__(256)
-k_pcg_update_lane(const int *__restrict__ lrow, int64_t ntiles, int nsteps, int TS,
-                  double *__restrict__ x, double *__restrict__ r, const double *__restrict__ s,
-                  const double *__restrict__ q, DevScalars *sc, double *__restrict__ rL,
-                  int64_t max_iters, double *history, HaloReset H) {
-    pdl_wait();
-    if (sc->done) return;
-    halo_reset(H, gtid(), gstride());
-    __shared__ double wm[8];
-    __shared__ bool last;
-    const double alpha = sc->alpha;
-    const int nchunk = (nsteps + kLaneRun - 1) / kLaneRun;
-    const int64_t items = ntiles * nchunk * TS;
-    double m = 0.0;
-    for (int64_t w = gtid(); w < items; w += gstride()) {
-        const int64_t p = w % TS, tc = w / TS;
-        const int64_t tile = tc / nchunk;
-        const int s0 = (int)(tc - tile * nchunk) * kLaneRun;
-        const int64_t e0 = (tile * nsteps + s0) * TS + p;
-        int rows[kLaneRun];
-#pragma unroll
-        for (int u = 0; u < kLaneRun; u++)
-            rows[u] = s0 + u < nsteps ? __ldg(lrow + e0 + (int64_t)u * TS) : -1;
-#pragma unroll
-        for (int u = 0; u < kLaneRun; u++) {
-            const int i = rows[u];
-            if (i < 0) continue;
-            x[i] = x[i] + alpha * s[i];
-            const double ri = r[i] - alpha * q[i];
-            r[i] = ri;
-            rL[e0 + (int64_t)u * TS] = ri;
-            m = fmax(m, fabs(ri));
-        }
-    }
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmax(m, wm[w]);
-        if (m > 0.0) atomic_max_nonneg(&sc->res_bits, m);
-        __threadfence();
-        last = atomicAdd(&sc->upd_ticket, 1u) == gridDim.x - 1;
-        if (last) {
-            sc->upd_ticket = 0u;
-            const double res = __longlong_as_double(
-                (long long)atomicAdd(&sc->res_bits, 0ull));
-            iter_check_body(sc, max_iters, history, res);
-        }
-    }
-}
-
 // convergence test after an iteration (pressure.py:324-326 / 211-213)
 __global__ void k_iter_check(DevScalars *sc, int64_t max_iters, double *history) {
     if (sc->done) return;
@@ -1413,7 +1355,6 @@ struct LaneBufs {
     LaneArgs args;       // geometry, halos, ticket, scale
     const int *posL;     // row -> L entry
     double *rL, *tqL, *zL, *preL;
-    const int *lrow = nullptr;  // L entry -> row (-1: none), k_lane_map
     HaloReset hr{};      // quad: per-direction halo buffers, reset by k_pcg_update
 };
 
@@ -1661,26 +1602,13 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                     solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
                     (*launches)++;
                 }
-                static const bool row_update = getenv("FLIPB200_ROW_UPDATE") != nullptr;
-                if (lane && !sl && LV.lane->lrow && !row_update) {
-                    const LaneBufs &Lb = *LV.lane;
-                    const WaveGeom &G = Lb.args.geom;
-                    const int TS = G.ty * G.tz;
-                    const int64_t items = (int64_t)G.TB * G.TC *
-                                          ((G.nsteps + kLaneRun - 1) / kLaneRun) * TS;
-                    launch_pdl(k_pcg_update_lane, wave_blocks(k_pcg_update_lane, items), kThreads,
-                               0, st, (const int *)Lb.lrow, (int64_t)G.TB * G.TC, G.nsteps, TS,
-                               B.x, B.r, (const double *)B.s, (const double *)B.q, sc, Lb.rL,
-                               (int64_t)cfg.max_iters, cfg.history, Lb.hr);
-                } else {
-                    launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
-                               B.x + o, B.r + o, (const double *)(B.s + o),
-                               (const double *)(B.q + o), sc,
-                               (lane && !sl) ? LV.lane->rL : nullptr,
-                               (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
-                               (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1,
-                               lane ? LV.lane->hr : HaloReset{});
-                }
+                launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
+                           B.x + o, B.r + o, (const double *)(B.s + o),
+                           (const double *)(B.q + o), sc,
+                           (lane && !sl) ? LV.lane->rL : nullptr,
+                           (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
+                           (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1,
+                           lane ? LV.lane->hr : HaloReset{});
                 if (sl) {
                     slab_max(cfg, &sc->res_bits);
                     k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
@@ -1923,7 +1851,6 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
             }
         }
         LB.posL = c.posL;
-        LB.lrow = c.lrow;
         LB.rL = c.laneA;
         LB.tqL = c.laneB;
         LB.zL = c.laneC;

@@ -444,7 +444,8 @@ static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     constexpr int QP = QT * QT, QW = 2 * QT;
     const int tiles = A.geom.TB * A.geom.TC;
     const size_t rings = ((size_t)A.geom.nsteps * 2 * QW * sizeof(double) + 127) / 128 * 128;
-    const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double);
+    static const size_t pad = getenv("FLIPB200_QUAD_PAD") ? (size_t)atoi(getenv("FLIPB200_QUAD_PAD")) * 1024 : 0;
+    const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double) + pad;
     static cudaError_t attr = [] {
         cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
