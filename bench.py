@@ -373,13 +373,18 @@ def run_ours(args):
         alg = pbytes.value / plaunch.value
         achieved = alg / (avg_ms / 1e3) / 1e9
         tr = load_traffic()
-        roof = {"bound": "hbm", "kernel": "k_mic_cl (MIC(0) substitution wavefront, DSMEM clusters, fwd+bwd)",
+        quad = os.environ.get("FLIPB200_QUAD", "1") != "0"
+        kname = ("k_mic_quad (MIC(0) substitution wavefront, 2x2 pencils per thread, DSMEM "
+                 "clusters, fwd+bwd)" if quad else
+                 "k_mic_cl (MIC(0) substitution wavefront, DSMEM clusters, fwd+bwd)")
+        roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_kind": peak_kind, "alg_bytes_per_launch": alg,
                 "avg_launch_ms": avg_ms, "launches_timed": int(plaunch.value),
                 "share_of_step": pms.value / ms,
                 # the ncu capture is of the 256^3 dam-break sweep
-                "traffic": ((tr or {}).get("k_mic_cl_dram_bytes_per_launch")
+                "traffic": ((tr or {}).get("k_mic_quad_dram_bytes_per_launch" if quad else
+                                           "k_mic_cl_dram_bytes_per_launch")
                             if (args.res, args.scene) == (256, "dam-break") else None),
                 "note": "latency-bound dependency wavefront (see DESIGN.md); "
                         "frac is of the HBM copy peak"}

@@ -249,6 +249,8 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
         if (fz) sq[1][z_q][z_row][z_col] = DZ < nsteps ? spin_z(DZ) : nz0;
         double py = (fy && 1 + DY < nsteps) ? peek_y(1 + DY) : nz0;
         double pz = (fz && 1 + DZ < nsteps) ? peek_z(1 + DZ) : nz0;
+        const int lag_g = (A.dbg >> 8) & 15, lag_s = (A.dbg >> 12) & 15;
+        double pyl = pend, pzl = pend;
         for (int s = 0; s < nsteps; s++) {
             __syncthreads();
             if (l == 0 && s > 0 && s % KC == 0 && !(A.dbg & 1)) {
@@ -257,13 +259,27 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
             }
             const int cur = s & 1;
             q_jitter(A.dbg, tile, s, t);
+            // lag (experiment, FLIPB200_QUAD_EXP bits 8-11 global / 12-15 DSMEM):
+            // keep the consumer LAG steps behind "just in time" by also waiting
+            // for the producer's slot s+1+D+LAG, so the prefetched slot is
+            // normally already valid
             if (fy) {
+                const int lag = iny ? lag_g : lag_s;
+                if (lag > 0 && s + 1 + DY + lag < nsteps) {
+                    if (is_pending(pyl)) pyl = spin_y(s + 1 + DY + lag);
+                    pyl = (s + 2 + DY + lag < nsteps) ? peek_y(s + 2 + DY + lag) : nz0;
+                }
                 double v = (s + 1 + DY < nsteps) ? py : nz0;
                 if (is_pending(v)) v = spin_y(s + 1 + DY);
                 sq[cur][y_q][y_row][y_col] = v;
                 py = (s + 2 + DY < nsteps) ? peek_y(s + 2 + DY) : nz0;
             }
             if (fz) {
+                const int lag = inz ? lag_g : lag_s;
+                if (lag > 0 && s + 1 + DZ + lag < nsteps) {
+                    if (is_pending(pzl)) pzl = spin_z(s + 1 + DZ + lag);
+                    pzl = (s + 2 + DZ + lag < nsteps) ? peek_z(s + 2 + DZ + lag) : nz0;
+                }
                 double v = (s + 1 + DZ < nsteps) ? pz : nz0;
                 if (is_pending(v)) v = spin_z(s + 1 + DZ);
                 sq[cur][z_q][z_row][z_col] = v;
