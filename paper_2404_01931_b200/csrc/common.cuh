@@ -39,6 +39,12 @@ __device__ __forceinline__ double div_dtau(const Dims &d, double x) {
     return d.pow2 ? x * d.inv_dtau : x / d.dtau;
 }
 
+// div_dtau with the power-of-two test resolved at compile time (hot loops)
+template <int P2>
+__device__ __forceinline__ double div_dtau_t(const Dims &d, double x) {
+    return P2 ? x * d.inv_dtau : x / d.dtau;
+}
+
 // (i, j, k) of cell c with 32-bit unsigned division (cell counts are below
 // 2^31, checked by flip_create).
 __device__ __forceinline__ void cell_ijk(const Dims &d, int64_t c, int &i, int &j, int &k) {
