@@ -14,10 +14,15 @@ the reference's own scene builder restated on the device (synthetic, seed 0).
 * e2e       the same metric through the C ABI with HOST buffers: every step
             uploads particles + labels from pinned host memory, steps, and
             downloads the particles.
-* roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_cl,
-            forward + backward, ~56% of the step): algorithmic bytes (3 x 8 B
-            per row) over the measured per-launch time (CUDA events
-            bracketing each launch on the library's stream).
+* roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_quad,
+            forward + backward, ~54% of the step): algorithmic bytes (3 x 8 B
+            per row) over the measured per-launch time of every launch in
+            the timed region.  The per-launch time comes from %globaltimer
+            stamps the kernel writes itself (first CTA past its programmatic
+            launch wait, last CTA exit): CUDA events recorded between the
+            launches would break the programmatic-dependent-launch overlap
+            of the PCG loop (measured: +3 ms per step).  The round-1
+            kernels (FLIPB200_QUAD=0) are still bracketed by CUDA events.
 * clocks    nvidia-smi every 50 ms from before the warm-up; only samples
             inside the timed region's wall-clock window are kept.
 * cpu_baseline  the oracle (C restatement of the reference step, all host
@@ -26,11 +31,14 @@ the reference's own scene builder restated on the device (synthetic, seed 0).
             reference cannot travel to the GPU box; oracle/ is its bit-exact
             C restatement, pinned by tests/).
 
-Multi-GPU (torchrun, one process per GPU, NCCL): the z-slab decomposition of
-paper_2404_01931_b200/dist.py -- particle stages sharded by slab (migration,
-ghost planes, owned-face all-gather, dt/label allreduces), the grid stages
-and the MIC(0)-PCG solve replicated.  The total workload stays the 256^3
-scene ("scaling": "strong"); results are bit-identical to one GPU.
+Multi-GPU (torchrun, one process per GPU, NCCL): the z-slab decomposition
+(csrc/slab.cu, driven from inside flip_step through paper_2404_01931_b200/
+dist.py's transport): every stage runs on the rank's planes / rows /
+particles with 1-plane halos, particle migration and ghost planes, MAX
+allreduces and the bit-exact distributed pairwise dot; the MIC(0) sweeps are
+one global recurrence, replicated on the all-gathered vector.
+The total workload stays the 256^3 scene ("scaling": "strong"); results are
+bit-identical to one GPU.
 """
 
 from __future__ import annotations
@@ -386,6 +394,9 @@ def run_ours(args):
                 "traffic": ((tr or {}).get("k_mic_quad_dram_bytes_per_launch" if quad else
                                            "k_mic_cl_dram_bytes_per_launch")
                             if (args.res, args.scene) == (256, "dam-break") else None),
+                "timing": ("in-kernel %globaltimer stamps per launch (first CTA start after "
+                           "the PDL wait, last CTA end), every launch of the timed region"
+                           if quad else "CUDA events bracketing each launch"),
                 "note": "latency-bound dependency wavefront (see DESIGN.md); "
                         "frac is of the HBM copy peak"}
 

@@ -211,6 +211,8 @@ extern "C" void flip_destroy(flip_ctx *c) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
+    if (c->probe.ts) cudaFree(c->probe.ts);
+    if (c->probe.ts_host) cudaFreeHost(c->probe.ts_host);
     for (auto &e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto &e : c->probe.ev)
@@ -815,10 +817,22 @@ extern "C" int flip_set_probe(flip_ctx *c, int32_t kind) {
     cudaSetDevice(c->device);
     if (kind && !c->probe.ev[0])
         for (auto &e : c->probe.ev) FLIP_CUDA_OK(cudaEventCreate(&e));
+    if (kind && !c->probe.ts) {
+        FLIP_CUDA_OK(cudaMalloc(&c->probe.ts, sizeof(unsigned long long) * 2 * kProbeSlots));
+        FLIP_CUDA_OK(cudaMallocHost(&c->probe.ts_host, sizeof(unsigned long long) * 2 * kProbeSlots));
+    }
+    if (c->probe.ts) {
+        FLIP_CUDA_OK(cudaMemsetAsync(c->probe.ts, 0xff, sizeof(unsigned long long) * kProbeSlots, c->st));
+        FLIP_CUDA_OK(cudaMemsetAsync(c->probe.ts + kProbeSlots, 0,
+                                     sizeof(unsigned long long) * kProbeSlots, c->st));
+    }
     c->probe.kind = kind;
     c->probe.used = 0;
     c->probe.bytes = 0.0;
     c->probe.launches = 0;
+    c->probe.stamp_ms = 0.0;
+    c->probe.stamp_bytes = 0.0;
+    c->probe.stamp_launches = 0;
     return 0;
 }
 
@@ -831,10 +845,12 @@ extern "C" int flip_get_probe(flip_ctx *c, double *total_ms, int64_t *launches, 
         FLIP_CUDA_OK(cudaEventElapsedTime(&ms, c->probe.ev[2 * k], c->probe.ev[2 * k + 1]));
         tot += ms;
     }
-    *total_ms = tot;
-    *launches = c->probe.used;
-    *bytes = c->probe.used == c->probe.launches ? c->probe.bytes
-                                                : c->probe.bytes * c->probe.used / c->probe.launches;
+    *total_ms = tot + c->probe.stamp_ms;
+    *launches = c->probe.used + c->probe.stamp_launches;
+    *bytes = (c->probe.used == c->probe.launches
+                  ? c->probe.bytes
+                  : c->probe.bytes * c->probe.used / c->probe.launches) +
+             c->probe.stamp_bytes;
     return 0;
 }
 

@@ -42,6 +42,12 @@ struct Probe {
     cudaEvent_t ev[2 * kMax]{};
     double bytes = 0.0;        // algorithmic bytes of the bracketed launches
     int64_t launches = 0;
+    // quad sweeps: device stamps instead of events (no event record between
+    // the kernels, so the probed step is the unprobed one; also works inside
+    // the solver graph).  ts: [kProbeSlots starts | kProbeSlots ends].
+    unsigned long long *ts = nullptr, *ts_host = nullptr;
+    double stamp_ms = 0.0, stamp_bytes = 0.0;
+    int64_t stamp_launches = 0;
 };
 
 // z-slab decomposition state (flip_set_slab_comm, slab.cu).  All arrays

@@ -1491,7 +1491,9 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 A.ticket = Lb.hr.ticket[rev];
                 A.prepped = fused ? 1 : 0;  // in the loop k_pcg_update reset them
             }
-            bool probed = pb && pb->kind == 1 && pb->used < Probe::kMax;
+            const bool stamped = pb && pb->kind == 1 && Lb.hr.on && pb->ts;  // quad: device stamps
+            if (stamped) A.ts = pb->ts;
+            bool probed = !stamped && pb && pb->kind == 1 && pb->used < Probe::kMax;
             if (probed) cudaEventRecord(pb->ev[2 * pb->used], st);
             cudaError_t e = launch_mic_lane(rev != 0, A, st);
             if (e != cudaSuccess) {
@@ -1517,6 +1519,50 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             S.n, r + o, cfg.precond == FLIP_PRECOND_JACOBI ? B.precon + o : nullptr, z + o, sc, 1);
         (*launches)++;
     }
+}
+
+// Device-driven solver loop: a graph holding one WHILE conditional node
+// whose body (captured from the stream) is one solver iteration followed by
+// k_loop_cond, which keeps the loop running while the done flag is clear.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const DevScalars *sc) {
+    pdl_wait();
+    cudaGraphSetConditional(h, sc->done ? 0u : 1u);
+}
+
+template <class F>
+static cudaError_t loop_graph(cudaStream_t st, const DevScalars *sc, int unroll, F &&body) {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t x = nullptr;
+    cudaGraphConditionalHandle h = 0;
+    cudaError_t e = cudaGraphCreate(&g, 0);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams np = {};
+    if (e == cudaSuccess) {
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        e = cudaGraphAddNode(&node, g, nullptr, 0, &np);
+    }
+    if (e == cudaSuccess) {
+        e = cudaStreamBeginCaptureToGraph(st, np.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeRelaxed);
+        if (e == cudaSuccess) {
+            for (int u = 0; u < unroll; u++) body();  // iterations past `done` exit at once
+            launch_pdl(k_loop_cond, 1, 1, 0, st, h, sc);
+            cudaGraph_t out = nullptr;
+            const cudaError_t e1 = cudaGetLastError();
+            const cudaError_t e2 = cudaStreamEndCapture(st, &out);
+            e = e1 != cudaSuccess ? e1 : e2;
+        }
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&x, g, 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(x, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the exec is destroyed below
+    if (x) cudaGraphExecDestroy(x);
+    if (g) cudaGraphDestroy(g);
+    return e;
 }
 
 // Runs SOLVERS[solver](sys, max_iters, tol) (pressure.py:200-332) on the
@@ -1580,94 +1626,129 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
         // gathered rhs (every rank then holds the same full iterate)
         slab_gather_rows(cfg, const_cast<double *>(S.rhs));
     }
-    int64_t it = 0, nbatch = 0, seen = 0;
-    while (nf > 0 && it < cfg.max_iters) {
-        int64_t batch = std::min<int64_t>(every, cfg.max_iters - it);
-        for (int64_t b = 0; b < batch; b++) {
-            if (!relax) {  // pressure.py:314-331
-                // r also lands in the lane layout and z comes back through the
-                // z.r dot (pressure.py:314-331); q = A s can be fused into the
-                // s.q dot too (FLIPB200_FUSE_MATVEC, slower: 8-lane groups
-                // coalesce the stencil gathers worse than k_matvec)
-                static const bool fuse_mv = getenv("FLIPB200_FUSE_MATVEC") != nullptr;
-                if (fuse_mv && !sl) {
-                    launch_dot_f(LdMatvecDot{S, B.s, B.q}, n, B.dot_tmp, nullptr, EPI_CURV, sc,
-                                 st, launches);
-                } else {
-                    if (S.meta)
-                        launch_pdl(k_matvec_c, wave_blocks(k_matvec_c, n), kThreads, 0, st, S, B.s, B.q, sc);
-                    else
-                        k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
-                                                                  nullptr, sc, 1);
-                    solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
-                    (*launches)++;
-                }
-                launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
-                           B.x + o, B.r + o, (const double *)(B.s + o),
-                           (const double *)(B.q + o), sc,
-                           (lane && !sl) ? LV.lane->rL : nullptr,
-                           (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
-                           (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1,
-                           lane ? LV.lane->hr : HaloReset{});
-                if (sl) {
-                    slab_max(cfg, &sc->res_bits);
-                    k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
-                    (*launches)++;
-                }
-                apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
-                if (lane)
-                    solver_dot(cfg, LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, nf, B.dot_tmp,
-                               EPI_SIGMA_NEW, sc, st, launches);
+    // one iteration of SOLVERS[cfg.solver] (pressure.py:209-213 / 314-331)
+    auto one_iter = [&]() {
+        if (!relax) {  // pressure.py:314-331
+            // r also lands in the lane layout and z comes back through the
+            // z.r dot (pressure.py:314-331); q = A s can be fused into the
+            // s.q dot too (FLIPB200_FUSE_MATVEC, slower: 8-lane groups
+            // coalesce the stencil gathers worse than k_matvec)
+            static const bool fuse_mv = getenv("FLIPB200_FUSE_MATVEC") != nullptr;
+            if (fuse_mv && !sl) {
+                launch_dot_f(LdMatvecDot{S, B.s, B.q}, n, B.dot_tmp, nullptr, EPI_CURV, sc,
+                             st, launches);
+            } else {
+                if (S.meta)
+                    launch_pdl(k_matvec_c, wave_blocks(k_matvec_c, n), kThreads, 0, st, S, B.s, B.q, sc);
                 else
-                    solver_dot(cfg, LdProd{B.z, B.r}, nf, B.dot_tmp, EPI_SIGMA_NEW, sc, st,
-                               launches);
-                launch_pdl(k_pcg_dir, wave_blocks(k_pcg_dir, n), kThreads, 0, st, n, B.s + o,
-                           (const double *)(B.z + o), (const DevScalars *)sc);
-                if (sl) slab_halo(cfg, B.s);
-                *launches += 2;  // update (with the convergence test) + dir
-            } else {  // pressure.py:209-213
-                if (cfg.solver == FLIP_SOLVER_JACOBI) {
-                    k_jacobi<<<nblocks(n), kThreads, 0, st>>>(S, B.x, B.xtmp, sc, 1);
-                    if (sl) slab_halo(cfg, B.xtmp);
-                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.xtmp, nullptr, S.rhs, &sc->res_bits,
-                                                              B.x, sc, 1);
-                    if (sl) {  // the halo rows of x follow xtmp's
-                        cudaMemcpyAsync(B.x + SL->Rlo, B.xtmp + SL->Rlo,
-                                        sizeof(double) * (SL->R0 - SL->Rlo), cudaMemcpyDeviceToDevice, st);
-                        cudaMemcpyAsync(B.x + SL->R1, B.xtmp + SL->R1,
-                                        sizeof(double) * (SL->Rhi - SL->R1), cudaMemcpyDeviceToDevice, st);
-                    }
-                    *launches += 2;
-                } else {
-                    bool gs_oop = cfg.solver == FLIP_SOLVER_GS && LV.wave;
-                    if (cfg.solver == FLIP_SOLVER_GS) {
-                        const SysView &F = sl ? *cfg.full : S;
-                        if (LV.wave) {  // out of place: old x in, new x out, copied back below
-                            do_sweep<SW_GS>(F, LV, B.x, B.xtmp, nullptr, sc, st, launches);
-                        } else {
-                            do_sweep<SW_GS>(F, LV, nullptr, B.x, nullptr, sc, st, launches);
-                        }
-                    } else {
-                        k_gs_rows<<<nblocks(cfg.red ? cfg.nred : n), kThreads, 0, st>>>(
-                            S, cfg.red, cfg.nred, 0, cfg.d, B.x, sc, 1);
-                        if (sl) slab_halo(cfg, B.x);
-                        k_gs_rows<<<nblocks(cfg.black ? cfg.nblack : n), kThreads, 0, st>>>(
-                            S, cfg.black, cfg.nblack, 1, cfg.d, B.x, sc, 1);
-                        if (sl) slab_halo(cfg, B.x);
-                        *launches += 2;
-                    }
-                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, gs_oop ? B.xtmp : B.x, nullptr,
-                                                              S.rhs, &sc->res_bits,
-                                                              (gs_oop && !sl) ? B.x : nullptr, sc, 1);
-                    if (gs_oop && sl)  // the replicated iterate, every row
-                        cudaMemcpyAsync(B.x, B.xtmp, sizeof(double) * nf, cudaMemcpyDeviceToDevice, st);
-                    (*launches)++;
-                }
-                if (sl) slab_max(cfg, &sc->res_bits);
+                    k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
+                                                              nullptr, sc, 1);
+                solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
+                (*launches)++;
+            }
+            launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
+                       B.x + o, B.r + o, (const double *)(B.s + o),
+                       (const double *)(B.q + o), sc,
+                       (lane && !sl) ? LV.lane->rL : nullptr,
+                       (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
+                       (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1,
+                       lane ? LV.lane->hr : HaloReset{});
+            if (sl) {
+                slab_max(cfg, &sc->res_bits);
                 k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
                 (*launches)++;
             }
+            apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
+            if (lane)
+                solver_dot(cfg, LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, nf, B.dot_tmp,
+                           EPI_SIGMA_NEW, sc, st, launches);
+            else
+                solver_dot(cfg, LdProd{B.z, B.r}, nf, B.dot_tmp, EPI_SIGMA_NEW, sc, st,
+                           launches);
+            launch_pdl(k_pcg_dir, wave_blocks(k_pcg_dir, n), kThreads, 0, st, n, B.s + o,
+                       (const double *)(B.z + o), (const DevScalars *)sc);
+            if (sl) slab_halo(cfg, B.s);
+            *launches += 2;  // update (with the convergence test) + dir
+        } else {  // pressure.py:209-213
+            if (cfg.solver == FLIP_SOLVER_JACOBI) {
+                k_jacobi<<<nblocks(n), kThreads, 0, st>>>(S, B.x, B.xtmp, sc, 1);
+                if (sl) slab_halo(cfg, B.xtmp);
+                k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.xtmp, nullptr, S.rhs, &sc->res_bits,
+                                                          B.x, sc, 1);
+                if (sl) {  // the halo rows of x follow xtmp's
+                    cudaMemcpyAsync(B.x + SL->Rlo, B.xtmp + SL->Rlo,
+                                    sizeof(double) * (SL->R0 - SL->Rlo), cudaMemcpyDeviceToDevice, st);
+                    cudaMemcpyAsync(B.x + SL->R1, B.xtmp + SL->R1,
+                                    sizeof(double) * (SL->Rhi - SL->R1), cudaMemcpyDeviceToDevice, st);
+                }
+                *launches += 2;
+            } else {
+                bool gs_oop = cfg.solver == FLIP_SOLVER_GS && LV.wave;
+                if (cfg.solver == FLIP_SOLVER_GS) {
+                    const SysView &F = sl ? *cfg.full : S;
+                    if (LV.wave) {  // out of place: old x in, new x out, copied back below
+                        do_sweep<SW_GS>(F, LV, B.x, B.xtmp, nullptr, sc, st, launches);
+                    } else {
+                        do_sweep<SW_GS>(F, LV, nullptr, B.x, nullptr, sc, st, launches);
+                    }
+                } else {
+                    k_gs_rows<<<nblocks(cfg.red ? cfg.nred : n), kThreads, 0, st>>>(
+                        S, cfg.red, cfg.nred, 0, cfg.d, B.x, sc, 1);
+                    if (sl) slab_halo(cfg, B.x);
+                    k_gs_rows<<<nblocks(cfg.black ? cfg.nblack : n), kThreads, 0, st>>>(
+                        S, cfg.black, cfg.nblack, 1, cfg.d, B.x, sc, 1);
+                    if (sl) slab_halo(cfg, B.x);
+                    *launches += 2;
+                }
+                k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, gs_oop ? B.xtmp : B.x, nullptr,
+                                                          S.rhs, &sc->res_bits,
+                                                          (gs_oop && !sl) ? B.x : nullptr, sc, 1);
+                if (gs_oop && sl)  // the replicated iterate, every row
+                    cudaMemcpyAsync(B.x, B.xtmp, sizeof(double) * nf, cudaMemcpyDeviceToDevice, st);
+                (*launches)++;
+            }
+            if (sl) slab_max(cfg, &sc->res_bits);
+            k_iter_check<<<1, 1, 0, st>>>(sc, cfg.max_iters, cfg.history);
+            (*launches)++;
         }
+    };
+    int64_t it = 0, nbatch = 0, seen = 0;
+    // FLIPB200_GRAPH=1 (one GPU): the whole loop is one CUDA graph -- a WHILE
+    // conditional node whose body is `unroll` iterations and whose condition
+    // (!done) is set on the device by the body's last kernel, so the host is
+    // not involved until the solve ends.  Measured 0.6 ms/step slower than
+    // the stream loop below at 256^3 (62.3 vs 61.7 ms; the per-solve capture
+    // and instantiation, and the WHILE round trips), so it is opt-in; the
+    // stream loop never drains the stream either (its done-flag reads are
+    // asynchronous).  The event probe needs the stream loop; the quad
+    // sweeps' device-stamp probe works in both.
+    static const bool graph_env = [] {
+        const char *e = getenv("FLIPB200_GRAPH");
+        return e ? atoi(e) != 0 : false;
+    }();
+    int64_t graph_per_iter = 0, graph_l0 = 0, graph_unroll = 1;  // launch accounting (graph mode)
+    const bool stamps = LV.probe && LV.probe->kind == 1 && LV.lane && LV.lane->hr.on && LV.probe->ts &&
+                        cfg.precond == FLIP_PRECOND_MIC0;
+    if (nf > 0 && !sl && graph_env && !(LV.probe && LV.probe->kind == 1 && !stamps)) {
+        // a body of `unroll` iterations: fewer WHILE round trips per solve
+        static const int unroll = [] {
+            const char *e = getenv("FLIPB200_GRAPH_UNROLL");
+            const int v = e ? atoi(e) : 4;
+            return v < 1 ? 1 : v > 64 ? 64 : v;
+        }();
+        graph_l0 = *launches;
+        graph_unroll = unroll;
+        cudaError_t ge = loop_graph(st, sc, unroll, one_iter);
+        graph_per_iter = (*launches - graph_l0) / unroll;
+        if (ge != cudaSuccess) {
+            set_error(std::string("solver graph: ") + cudaGetErrorString(ge));
+            return FLIP_E_CUDA;
+        }
+        it = cfg.max_iters;  // the device ran the loop to its end
+    }
+    while (nf > 0 && it < cfg.max_iters) {
+        int64_t batch = std::min<int64_t>(every, cfg.max_iters - it);
+        for (int64_t b = 0; b < batch; b++) one_iter();
         it += batch;
         if (sl) {  // every rank polls after the same batch (the batches hold collectives)
             cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
@@ -1703,6 +1784,28 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
     FLIP_CUDA_OK(cudaStreamSynchronize(st));
     FLIP_CUDA_OK(cudaGetLastError());
+    if (graph_per_iter) {  // body executions x (its iterations' kernels + the loop test)
+        const int64_t bodies = std::max<int64_t>(1, (sch->iter + graph_unroll - 1) / graph_unroll);
+        *launches = graph_l0 + bodies * (graph_unroll * graph_per_iter + 1);
+    }
+    if (stamps && !relax) {  // this solve's sweep durations, then re-arm the slots
+        Probe &pb = *LV.probe;
+        const int used = (int)std::min<int64_t>(2 * (sch->iter + 1), kProbeSlots);
+        FLIP_CUDA_OK(cudaMemcpyAsync(pb.ts_host, pb.ts, sizeof(unsigned long long) * used,
+                                     cudaMemcpyDeviceToHost, st));
+        FLIP_CUDA_OK(cudaMemcpyAsync(pb.ts_host + kProbeSlots, pb.ts + kProbeSlots,
+                                     sizeof(unsigned long long) * used, cudaMemcpyDeviceToHost, st));
+        FLIP_CUDA_OK(cudaStreamSynchronize(st));
+        for (int k = 0; k < used; k++) {
+            const unsigned long long a = pb.ts_host[k], b = pb.ts_host[kProbeSlots + k];
+            if (a == ~0ull || b == 0ull || b < a) continue;
+            pb.stamp_ms += (double)(b - a) * 1e-6;
+            pb.stamp_launches++;
+            pb.stamp_bytes += 24.0 * (double)nf;  // src + precon read, dst written per row
+        }
+        cudaMemsetAsync(pb.ts, 0xff, sizeof(unsigned long long) * kProbeSlots, st);
+        cudaMemsetAsync(pb.ts + kProbeSlots, 0, sizeof(unsigned long long) * kProbeSlots, st);
+    }
     out->iterations = sch->iter;
     out->residual = sch->res;
     out->converged = sch->converged;

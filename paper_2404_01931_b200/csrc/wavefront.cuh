@@ -160,7 +160,12 @@ struct LaneArgs {
     unsigned long long *trace;  // optional per-step clock of tile 0 lane 0
     int dbg;                    // traced tile index (FLIPB200_LANE_DBG, with FLIPB200_WAVE_TRACE)
     int prepped = 0;            // quad: halo + ticket already reset (by k_pcg_update)
+    // probe (quad): per-launch [first CTA start, last CTA end] %globaltimer
+    // stamps, starts at ts[slot], ends at ts[kProbeSlots + slot], slot =
+    // 2 * iteration + direction
+    unsigned long long *ts = nullptr;
 };
+constexpr int kProbeSlots = 1024;
 
 // Reset of the quad sweeps' cross-cluster halo slots and tickets, folded
 // into the kernel that precedes the forward sweep (k_pcg_update) instead of

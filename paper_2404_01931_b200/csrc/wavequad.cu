@@ -151,6 +151,14 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
     const int t = threadIdx.x;
     pdl_wait();
     if (A.sc && A.sc->done) return;
+    // probe: this launch's slot (the iteration counter is final before the
+    // sweeps run: k_pcg_update advanced it)
+    const int pslot = A.ts ? min(2 * (A.sc ? A.sc->iter : 0) + (REV ? 1 : 0), kProbeSlots - 1) : 0;
+    if (A.ts && t == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        atomicMin(A.ts + pslot, g);
+    }
     const WaveGeom G = A.geom;
     const int nsteps = G.nsteps;
     double *yring = ring, *zring = ring + (int64_t)nsteps * QW;
@@ -389,6 +397,11 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
         }
     }
     q_cluster_sync();  // no CTA leaves while a peer can still store into its rings
+    if (A.ts && t == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        atomicMax(A.ts + kProbeSlots + pslot, g);
+    }
 }
 
 // ------------------------------------------------------------- launching --
