@@ -160,6 +160,9 @@ struct LaneArgs {
     unsigned long long *trace;  // optional per-step clock of tile 0 lane 0
     int dbg;                    // traced tile index (FLIPB200_LANE_DBG, with FLIPB200_WAVE_TRACE)
     int prepped = 0;            // quad: halo + ticket already reset (by k_pcg_update)
+    int pf = 1;                 // quad: face values loaded ahead by the helper warp
+    int hw = 1;                 // quad: helper warps (2: one per face)
+    int trace_t0 = 0;           // quad trace: first of the 8 tiles with per-step stamps
     // probe (quad): per-launch [first CTA start, last CTA end] %globaltimer
     // stamps, starts at ts[slot], ends at ts[kProbeSlots + slot], slot =
     // 2 * iteration + direction

@@ -134,8 +134,8 @@ __device__ __forceinline__ double mic_cell(double a, double pr, double pv, doubl
 
 // QT threads per tile edge (16 or 8): a tile is 2QT x 2QT pencils, the
 // faces are QW = 2QT values wide.
-template <bool REV, int QT, int CY, int CZ, int KC, int NB>
-__global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
+template <bool REV, int QT, int CY, int CZ, int KC, int NB, int PF, int HW = 1>
+__global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
     constexpr int QP = QT * QT, QW = 2 * QT;
     constexpr int DY = QT - 1, DZ = QT - 1;
     // logical cell L (forward order (0,0), (1,0), (0,1), (1,1)) -> stored q
@@ -216,10 +216,15 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
         // lane l carries y-face word l (consumer kk = l/2; e = 0 feeds
         // logical cell 0, e = 1 cell 2) and z-face word l (consumer jj =
         // l/2; e = 0 feeds cell 0, e = 1 cell 1)
-        const int l = t - QP;
-        // y word ly and z word lz of this lane (-1: none)
-        const int ly = QW == 32 ? l : (l < QW ? l : -1);
-        const int lz = QW == 32 ? l : (l >= 32 - QW ? l - (32 - QW) : -1);
+        const int l = (t - QP) & 31;
+        // y word ly and z word lz of this lane (-1: none).  HW = 2: one
+        // helper warp per face (y: the first, z: the second), so a tile fed
+        // on both faces does not run the two faces' waits one after the
+        // other in divergent halves of one warp.
+        const int hw = (t - QP) >> 5;
+        const int ly = HW == 2 ? (hw == 0 && l < QW ? l : -1) : QW == 32 ? l : (l < QW ? l : -1);
+        const int lz = HW == 2 ? (hw == 1 && l < QW ? l : -1)
+                               : QW == 32 ? l : (l >= 32 - QW ? l - (32 - QW) : -1);
         // The helper also forwards the faces that arrive by DSMEM (from its
         // own rings), so no compute lane polls or diverges on face code
         // (measured: 176.4 -> 169.2 us per sweep at 256^3).
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
         const int cons_j = REV ? QT - 1 : 0, cons_k = REV ? QT - 1 : 0;
         if (!(G.jlo + b * QW + 2 * cons_j <= G.jhi && G.klo + c * QW + 2 * hy_ <= G.khi)) iny = ly_ring = nullptr;
         if (!(G.jlo + b * QW + 2 * hz_ <= G.jhi && G.klo + c * QW + 2 * cons_k <= G.khi)) inz = lz_ring = nullptr;
-        if (l == 0)
+        if (l == 0 && hw == 0)
             for (int q = 0; q < NB; q++) issue(q);
         // slot of producer step sp: global halo or local DSMEM ring
         auto peek_y = [&](int sp) { return iny ? ld_relaxed(iny + (int64_t)sp * QW) : q_peek(ly_ring + sp * QW); };
@@ -255,43 +260,53 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
         const bool fy = iny || ly_ring, fz = inz || lz_ring;
         if (fy) sq[1][y_q][y_row][y_col] = DY < nsteps ? spin_y(DY) : nz0;
         if (fz) sq[1][z_q][z_row][z_col] = DZ < nsteps ? spin_z(DZ) : nz0;
-        double py = (fy && 1 + DY < nsteps) ? peek_y(1 + DY) : nz0;
-        double pz = (fz && 1 + DZ < nsteps) ? peek_z(1 + DZ) : nz0;
-        const int lag_g = (A.dbg >> 8) & 15, lag_s = (A.dbg >> 12) & 15;
-        double pyl = pend, pzl = pend;
-        for (int s = 0; s < nsteps; s++) {
-            __syncthreads();
-            if (l == 0 && s > 0 && s % KC == 0 && !(A.dbg & 1)) {
-                fence_proxy_async();
-                issue(s / KC - 1 + NB);
-            }
-            const int cur = s & 1;
-            q_jitter(A.dbg, tile, s, t);
-            // lag (experiment, FLIPB200_QUAD_EXP bits 8-11 global / 12-15 DSMEM):
-            // keep the consumer LAG steps behind "just in time" by also waiting
-            // for the producer's slot s+1+D+LAG, so the prefetched slot is
-            // normally already valid
-            if (fy) {
-                const int lag = iny ? lag_g : lag_s;
-                if (lag > 0 && s + 1 + DY + lag < nsteps) {
-                    if (is_pending(pyl)) pyl = spin_y(s + 1 + DY + lag);
-                    pyl = (s + 2 + DY + lag < nsteps) ? peek_y(s + 2 + DY + lag) : nz0;
+        // Face values of the next PF steps are loaded ahead: a global-halo
+        // load takes ~0.6 us, longer than a step, so with one load in flight
+        // a tile fed across a cluster boundary steps at the load latency
+        // (trace: 0.55-0.65 us per step there vs 0.23-0.3 inside a
+        // cluster).  The loop is unrolled by PF so every queued register is
+        // read only when its slot is consumed (a rotating queue would wait
+        // for all loads in flight at every step).
+        double qy[PF], qz[PF];
+#pragma unroll
+        for (int u = 0; u < PF; u++) {
+            qy[u] = (fy && 1 + u + DY < nsteps) ? peek_y(1 + u + DY) : nz0;
+            qz[u] = (fz && 1 + u + DZ < nsteps) ? peek_z(1 + u + DZ) : nz0;
+        }
+        for (int s0 = 0; s0 < nsteps; s0 += PF) {
+#pragma unroll
+            for (int u = 0; u < PF; u++) {
+                const int s = s0 + u;
+                if (s >= nsteps) break;
+                __syncthreads();
+                if (l == 0 && hw == 0 && s > 0 && s % KC == 0 && !(A.dbg & 1)) {
+                    fence_proxy_async();
+                    issue(s / KC - 1 + NB);
                 }
-                double v = (s + 1 + DY < nsteps) ? py : nz0;
-                if (is_pending(v)) v = spin_y(s + 1 + DY);
-                sq[cur][y_q][y_row][y_col] = v;
-                py = (s + 2 + DY < nsteps) ? peek_y(s + 2 + DY) : nz0;
-            }
-            if (fz) {
-                const int lag = inz ? lag_g : lag_s;
-                if (lag > 0 && s + 1 + DZ + lag < nsteps) {
-                    if (is_pending(pzl)) pzl = spin_z(s + 1 + DZ + lag);
-                    pzl = (s + 2 + DZ + lag < nsteps) ? peek_z(s + 2 + DZ + lag) : nz0;
+                const int cur = s & 1;
+                q_jitter(A.dbg, tile, s, t);
+                if (fy) {
+                    double v = (s + 1 + DY < nsteps) ? qy[u] : nz0;
+                    if (is_pending(v)) {
+                        v = spin_y(s + 1 + DY);
+                        const int trel = tile - A.trace_t0;
+                        if (trace && trel >= 0 && trel < 8 && s < 300)
+                            atomicOr(trace + 24000 + trel * 300 + s, iny ? 1ull : 4ull);
+                    }
+                    sq[cur][y_q][y_row][y_col] = v;
+                    qy[u] = (s + 1 + PF + DY < nsteps) ? peek_y(s + 1 + PF + DY) : nz0;
                 }
-                double v = (s + 1 + DZ < nsteps) ? pz : nz0;
-                if (is_pending(v)) v = spin_z(s + 1 + DZ);
-                sq[cur][z_q][z_row][z_col] = v;
-                pz = (s + 2 + DZ < nsteps) ? peek_z(s + 2 + DZ) : nz0;
+                if (fz) {
+                    double v = (s + 1 + DZ < nsteps) ? qz[u] : nz0;
+                    if (is_pending(v)) {
+                        v = spin_z(s + 1 + DZ);
+                        const int trel = tile - A.trace_t0;
+                        if (trace && trel >= 0 && trel < 8 && s < 300)
+                            atomicOr(trace + 24000 + trel * 300 + s, inz ? 2ull : 8ull);
+                    }
+                    sq[cur][z_q][z_row][z_col] = v;
+                    qz[u] = (s + 1 + PF + DZ < nsteps) ? peek_z(s + 1 + PF + DZ) : nz0;
+                }
             }
         }
         __syncthreads();
@@ -331,10 +346,11 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
                 if (u >= cnt) break;
                 const int s = s0 + u;
                 __syncthreads();
-                if (trace && t == 0 && (s == 0 || (tile < 8 && s < 300))) {
+                const int trel = tile - A.trace_t0;  // per-step stamps of 8 tiles
+                if (trace && t == 0 && (s == 0 || (trel >= 0 && trel < 8 && s < 300))) {
                     unsigned long long g;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-                    if (tile < 8 && s < 300) trace[20000 + tile * 300 + s] = g;
+                    if (trel >= 0 && trel < 8 && s < 300) trace[20000 + trel * 300 + s] = g;
                     if (s == 0) trace[4 * tile + 2] = g;
                 }
                 const int cur = s & 1, prv = cur ^ 1;
@@ -407,6 +423,13 @@ __global__ void __launch_bounds__(QT * QT + 32) k_mic_quad(LaneArgs A) {
 // ------------------------------------------------------------- launching --
 int quad_threads();
 
+// Helper warps per CTA (FLIPB200_QUAD_HW): 2 = one per face (measured at
+// 256^3: 0.167 -> 0.118 ms per sweep), 1 = round-2's single helper warp.
+static int hw_default() {
+    static const int hw = getenv("FLIPB200_QUAD_HW") ? atoi(getenv("FLIPB200_QUAD_HW")) : 2;
+    return hw == 1 ? 1 : 2;
+}
+
 int quad_cluster_shape(int *cy, int *cz) {
     static int y = -1, z = -1;
     if (y < 0) {
@@ -468,7 +491,7 @@ WaveGeom quad_geom(const int lo[3], const int hi[3]) {
     return g;
 }
 
-template <bool REV, int QT, int CY, int CZ, int KC, int NB>
+template <bool REV, int QT, int CY, int CZ, int KC, int NB, int PF = 1, int HW = 1>
 static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     constexpr int QP = QT * QT, QW = 2 * QT;
     const int tiles = A.geom.TB * A.geom.TC;
@@ -476,11 +499,11 @@ static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     static const size_t pad = getenv("FLIPB200_QUAD_PAD") ? (size_t)atoi(getenv("FLIPB200_QUAD_PAD")) * 1024 : 0;
     const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double) + pad;
     static cudaError_t attr = [] {
-        cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB>,
+        cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024 - 24 * 1024);
         if (e == cudaSuccess && CY * CZ > 8)
-            e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB>,
+            e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         return e;
     }();
@@ -488,7 +511,7 @@ static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     if (smem > 227 * 1024 - 24 * 1024) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)tiles);
-    cfg.blockDim = dim3(QP + 32);
+    cfg.blockDim = dim3(QP + 32 * HW);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -500,18 +523,18 @@ static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_quad<REV, QT, CY, CZ, KC, NB>, A);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW>, A);
     return e != cudaSuccess ? e : cudaPeekAtLastError();
 }
 
 // Can the configured quad kernel's clusters be scheduled on this device
 // (16-CTA clusters are non-portable)?  Checked once per process.
-template <int QT, int CY, int CZ, int KC, int NB>
+template <int QT, int CY, int CZ, int KC, int NB, int HW = 1>
 static bool quad_fits(int nsteps) {
     constexpr int QP = QT * QT, QW = 2 * QT;
     const size_t rings = ((size_t)nsteps * 2 * QW * sizeof(double) + 127) / 128 * 128;
     const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double);
-    auto k = k_mic_quad<false, QT, CY, CZ, KC, NB>;
+    auto k = k_mic_quad<false, QT, CY, CZ, KC, NB, 1, HW>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024 - 24 * 1024) != cudaSuccess)
         return false;
@@ -520,7 +543,7 @@ static bool quad_fits(int nsteps) {
         return false;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CY * CZ);
-    cfg.blockDim = dim3(QP + 32);
+    cfg.blockDim = dim3(QP + 32 * HW);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -558,7 +581,15 @@ static cudaError_t launch_quad_c(const LaneArgs &A, cudaStream_t st) {
         case 404: return launch_quad_k<REV, 8, CY, CZ, 4, 4>(A, st);
         case 803: return launch_quad_k<REV, 8, CY, CZ, 8, 3>(A, st);
         case 1602: return launch_quad_k<REV, 8, CY, CZ, 16, 2>(A, st);
-        default: return launch_quad_k<REV, 8, CY, CZ, 8, 2>(A, st);
+        default:
+            switch (A.pf * 10 + A.hw) {  // FLIPB200_QUAD_PF, FLIPB200_QUAD_HW
+                case 21: return launch_quad_k<REV, 8, CY, CZ, 8, 2, 2, 1>(A, st);
+                case 31: return launch_quad_k<REV, 8, CY, CZ, 8, 2, 3, 1>(A, st);
+                case 12: return launch_quad_k<REV, 8, CY, CZ, 8, 2, 1, 2>(A, st);
+                case 22: return launch_quad_k<REV, 8, CY, CZ, 8, 2, 2, 2>(A, st);
+                case 32: return launch_quad_k<REV, 8, CY, CZ, 8, 2, 3, 2>(A, st);
+                default: return launch_quad_k<REV, 8, CY, CZ, 8, 2, 1, 1>(A, st);
+            }
     }
 }
 
@@ -566,6 +597,14 @@ cudaError_t launch_mic_quad(bool rev, const LaneArgs &A0, cudaStream_t st) {
     static const int exp_flags = getenv("FLIPB200_QUAD_EXP") ? atoi(getenv("FLIPB200_QUAD_EXP")) : 0;
     LaneArgs A = A0;
     A.dbg = exp_flags;
+    static const int pf = [] {  // global-face prefetch depth (FLIPB200_QUAD_PF)
+        const char *e = getenv("FLIPB200_QUAD_PF");
+        return e ? atoi(e) : 1;
+    }();
+    A.pf = pf;
+    A.hw = hw_default();
+    static const int t0 = getenv("FLIPB200_TRACE_TILE0") ? atoi(getenv("FLIPB200_TRACE_TILE0")) : 0;
+    A.trace_t0 = t0;
     int cy, cz;
     quad_cluster_shape(&cy, &cz);
     if (!A.geom.quad || A.geom.TB % cy || A.geom.TC % cz) return cudaErrorNotSupported;
@@ -589,7 +628,7 @@ bool mic_quad_supported(int nsteps) {
     const int key = cy * 100 + cz;
     // the default shape / chunking of each tile edge (what launch_quad_c picks)
     if (quad_threads() == 8 && key == 404 && (quad_chunks() == 0 || quad_chunks() == 802))
-        return quad_fits<8, 4, 4, 8, 2>(nsteps);
+        return hw_default() == 2 ? quad_fits<8, 4, 4, 8, 2, 2>(nsteps) : quad_fits<8, 4, 4, 8, 2, 1>(nsteps);
     if (quad_threads() == 16 && key == 204) return quad_fits<16, 2, 4, 2, 3>(nsteps);
     return cy * cz <= 16;  // other (experimental) shapes: the launch reports misfits
 }
