@@ -828,11 +828,21 @@ __global__ void k_lane_map(WaveGeom G, Dims d, int TY, int TZ, const uint8_t *__
     const double ab = __longlong_as_double((long long)WAVE_ABSENT);
     for (int64_t e = gtid(); e < nL; e += gstride()) {
         // 32-bit decomposition: lane entries stay below 2^31 (lane_entries_max)
-        const unsigned ue = (unsigned)e, ts = ue / (unsigned)TP;
-        int p = (int)(ue - ts * (unsigned)TP);
-        const unsigned tq = ts / (unsigned)G.nsteps;
-        int s = (int)(ts - tq * (unsigned)G.nsteps);
-        int tile = (int)tq;
+        const unsigned ue = (unsigned)e;
+        int p, s, tile;
+        if (G.quad) {  // ((tile * nsteps/4 + g) * TP + p) * 4 + w, step 4g + w
+            const unsigned r = ue >> 2, tg = r / (unsigned)TP, ng = (unsigned)G.nsteps >> 2;
+            p = (int)(r - tg * (unsigned)TP);
+            const unsigned tq = tg / ng;
+            s = 4 * (int)(tg - tq * ng) + (int)(ue & 3u);
+            tile = (int)tq;
+        } else {
+            const unsigned ts = ue / (unsigned)TP;
+            p = (int)(ue - ts * (unsigned)TP);
+            const unsigned tq = ts / (unsigned)G.nsteps;
+            s = (int)(ts - tq * (unsigned)G.nsteps);
+            tile = (int)tq;
+        }
         int b = tile / G.TC, c = tile % G.TC;
         int i, j, k;
         if (G.quad) {  // [q][thread]: thread (jj, kk) of QT x QT owns pencils (2jj + a, 2kk + b)

@@ -15,9 +15,9 @@
 //
 // Arithmetic and operation order per cell are k_mic_cl's (absent
 // neighbours are -0.0, an exact no-op), so results are bit-identical.
-// Lane layout (k_lane_map with quad geometry): L[tile][step][q][thread],
-// q = a + 2b, i.e. 1024 entries per tile-step, one coalesced 8-byte load
-// per thread per q.
+// Lane layout (k_lane_map with quad geometry): L[tile][step/4][q][thread]
+// [step%4], q = a + 2b: 256 entries per tile-step, in groups of 4 steps so
+// that consecutive rows of a pencil share a sector.
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -128,6 +128,27 @@ __device__ __forceinline__ double mic_cell(double a, double pr, double pv, doubl
         double tt = ((a + sp * pv) + sp * yv) + sp * zv;
         o = tt * pr;
         if (dst) __stcg(dst, row ? o : absent);
+    }
+    return row ? o : -0.0;
+}
+
+// mic_cell returning the lane-layout value (the row's result, or the ABSENT
+// marker) instead of storing it: the quad kernel stores 4 steps at once.
+template <bool REV>
+__device__ __forceinline__ double mic_cell_v(double a, double pr, double pv, double yv, double zv,
+                                             double sc, bool row, double &stored) {
+    const double absent = __longlong_as_double((long long)WAVE_ABSENT);
+    double o;
+    if (!REV) {  // _core.pyx:322-332
+        double tt = ((a + pv) + yv) + zv;
+        double q = tt * pr;
+        stored = row ? q : absent;
+        o = (sc * pr) * q;
+    } else {     // _core.pyx:333-346
+        double sp = sc * pr;
+        double tt = ((a + sp * pv) + sp * yv) + sp * zv;
+        o = tt * pr;
+        stored = row ? o : absent;
     }
     return row ? o : -0.0;
 }
@@ -329,79 +350,119 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
         const unsigned zout = (zdout && kk == prod_k) ? q_map(zring + 2 * jj, cr + 1) : 0u;
         double *gy = (!ydout && jj == prod_j) ? A.halo_y + (int64_t)tile * nsteps * QW + 2 * kk : nullptr;
         double *gz = (!zdout && kk == prod_k) ? A.halo_z + (int64_t)tile * nsteps * QW + 2 * jj : nullptr;
-        const int64_t base = (int64_t)tile * nsteps * TS + t;
-        double *dstL = A.dst + base;
+        // lane layout, groups of 4 steps: entry ((g * TS + q * QP + t) * 4 + w)
+        // for step 4g + w of the tile (k_lane_map), so 4 consecutive steps of
+        // a pencil share one 32-byte sector (the PCG update's r scatter and
+        // the z.r dot's gather touch a quarter of the sectors)
+        double *dstL = A.dst + (int64_t)tile * nsteps * TS + 4 * t;
         double pv[4] = {nz0, nz0, nz0, nz0};
         const double sc = A.scale;
         const int yr = kk + 1, yc = jj + nbo, zr = kk + nbo, zc = jj + 1;
         const int X = A.dbg;  // timing experiments only (FLIPB200_QUAD_EXP): results differ
+        // Per chunk, groups of 4 steps: a group's operands are in registers
+        // before its first step (two 16-byte shared loads per cell and
+        // array); the next group's are issued one cell per step during the
+        // current group, behind that step's neighbour reads.  Outputs are
+        // stored per group (16-byte stores).
         for (int ch = 0; ch < nch; ch++) {
-            const int s0 = ch * KC, cnt = min(KC, nsteps - s0);
+            const int s0 = ch * KC, cnt = min(KC, nsteps - s0);  // cnt: a multiple of 4
             const int buf = ch % NB;
             if (!(X & 1) || ch < NB) mbar_wait(&mbar[buf], (unsigned)(ch / NB) & 1u);
-            const double *ab = opb + (buf * 2 + 0) * KC * TS + t;
-            const double *pb = opb + (buf * 2 + 1) * KC * TS + t;
+            const double *ab = opb + (buf * 2 + 0) * KC * TS + 4 * t;
+            const double *pb = opb + (buf * 2 + 1) * KC * TS + 4 * t;
+            const int lo = REV ? nsteps - s0 - cnt : s0;  // the chunk holds logical steps [lo, lo + cnt)
+            const int ng = cnt / 4;
+            auto load_cell = [&](int gi, int L, double2 (&AA)[4][2], double2 (&PP)[4][2]) {
+                const int g = REV ? ng - 1 - gi : gi;  // group in the buffer
+                const double *pa = ab + (g * TS + PQ(L) * QP) * 4;
+                const double *pp = pb + (g * TS + PQ(L) * QP) * 4;
+                AA[L][0] = *reinterpret_cast<const double2 *>(pa);
+                AA[L][1] = *reinterpret_cast<const double2 *>(pa + 2);
+                PP[L][0] = *reinterpret_cast<const double2 *>(pp);
+                PP[L][1] = *reinterpret_cast<const double2 *>(pp + 2);
+            };
+            double2 A2[4][2], P2[4][2], NA[4][2], NP[4][2];
 #pragma unroll
-            for (int u = 0; u < KC; u++) {
-                if (u >= cnt) break;
-                const int s = s0 + u;
-                __syncthreads();
-                const int trel = tile - A.trace_t0;  // per-step stamps of 8 tiles
-                if (trace && t == 0 && (s == 0 || (trel >= 0 && trel < 8 && s < 300))) {
-                    unsigned long long g;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-                    if (trel >= 0 && trel < 8 && s < 300) trace[20000 + trel * 300 + s] = g;
-                    if (s == 0) trace[4 * tile + 2] = g;
-                }
-                const int cur = s & 1, prv = cur ^ 1;
-                const int idx = REV ? cnt - 1 - u : u;
-                double a[4], pr[4];
+            for (int L = 0; L < 4; L++) load_cell(0, L, A2, P2);
 #pragma unroll
-                for (int L = 0; L < 4; L++) {
-                    a[L] = ab[idx * TS + PQ(L) * QP];
-                    pr[L] = pb[idx * TS + PQ(L) * QP];
-                }
-                // neighbour contributions from the previous step: -y feeds
-                // logical cells 0 and 2 (the -y thread's cells 1 and 3), -z
-                // feeds cells 0 and 1 (the -z thread's cells 2 and 3)
-                double y0 = sq[prv][PQ(1)][yr][yc], y2 = sq[prv][PQ(3)][yr][yc];
-                double z0 = sq[prv][PQ(2)][zr][zc], z1 = sq[prv][PQ(3)][zr][zc];
-                double *d = dstL + (int64_t)lstep(s) * TS;
-                const bool nost = X & 2;
-                double o[4];
-                if (X & 4) {
+            for (int gi = 0; gi < KC / 4; gi++) {
+                if (gi >= ng) break;
+                const int g = REV ? ng - 1 - gi : gi;  // group in the buffer
+                if (gi > 0) {
 #pragma unroll
-                    for (int L = 0; L < 4; L++) o[L] = a[L] + pr[L];
-                    o[0] = o[0] + y0 + z0;
-                    o[1] = o[1] + z1;
-                    o[2] = o[2] + y2;
-                } else {
-                o[0] = mic_cell<REV>(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), nost ? nullptr : d + PQ(0) * QP);
-                o[1] = mic_cell<REV>(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), nost ? nullptr : d + PQ(1) * QP);
-                o[2] = mic_cell<REV>(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), nost ? nullptr : d + PQ(2) * QP);
-                o[3] = mic_cell<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), nost ? nullptr : d + PQ(3) * QP);
+                    for (int L = 0; L < 4; L++) {
+                        A2[L][0] = NA[L][0];
+                        A2[L][1] = NA[L][1];
+                        P2[L][0] = NP[L][0];
+                        P2[L][1] = NP[L][1];
+                    }
                 }
+                double O[4][4];  // stored values [cell][step in the group, logical order]
 #pragma unroll
-                for (int L = 0; L < 4; L++) {
-                    sq[cur][PQ(L)][kk + 1][jj + 1] = o[L];
-                    pv[L] = o[L];
+                for (int u = 0; u < 4; u++) {
+                    const int s = s0 + 4 * gi + u;
+                    const int w = REV ? 3 - u : u;  // logical step within the group
+                    __syncthreads();
+                    const int trel = tile - A.trace_t0;  // per-step stamps of 8 tiles
+                    if (trace && t == 0 && (s == 0 || (trel >= 0 && trel < 8 && s < 300))) {
+                        unsigned long long gt;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+                        if (trel >= 0 && trel < 8 && s < 300) trace[20000 + trel * 300 + s] = gt;
+                        if (s == 0) trace[4 * tile + 2] = gt;
+                    }
+                    const int cur = s & 1, prv = cur ^ 1;
+                    double a[4], pr[4];
+#pragma unroll
+                    for (int L = 0; L < 4; L++) {
+                        const double2 av = A2[L][w >> 1], pv2 = P2[L][w >> 1];
+                        a[L] = (w & 1) ? av.y : av.x;
+                        pr[L] = (w & 1) ? pv2.y : pv2.x;
+                    }
+                    // neighbour contributions from the previous step: -y feeds
+                    // logical cells 0 and 2 (the -y thread's cells 1 and 3), -z
+                    // feeds cells 0 and 1 (the -z thread's cells 2 and 3)
+                    const double y0 = sq[prv][PQ(1)][yr][yc], y2 = sq[prv][PQ(3)][yr][yc];
+                    const double z0 = sq[prv][PQ(2)][zr][zc], z1 = sq[prv][PQ(3)][zr][zc];
+                    if (gi + 1 < ng) {
+                        asm volatile("" ::: "memory");
+                        load_cell(gi + 1, u, NA, NP);
+                        asm volatile("" ::: "memory");
+                    }
+                    double o[4];
+                    o[0] = mic_cell_v<REV>(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), O[0][w]);
+                    o[1] = mic_cell_v<REV>(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), O[1][w]);
+                    o[2] = mic_cell_v<REV>(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), O[2][w]);
+                    o[3] = mic_cell_v<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), O[3][w]);
+#pragma unroll
+                    for (int L = 0; L < 4; L++) {
+                        sq[cur][PQ(L)][kk + 1][jj + 1] = o[L];
+                        pv[L] = o[L];
+                    }
+                    q_jitter(X, tile, s, t);
+                    if (yout) {
+                        q_st_remote(yout + (unsigned)(s * QW * 8), o[1]);
+                        q_st_remote(yout + (unsigned)(s * QW * 8 + 8), o[3]);
+                    }
+                    if (zout) {
+                        q_st_remote(zout + (unsigned)(s * QW * 8), o[2]);
+                        q_st_remote(zout + (unsigned)(s * QW * 8 + 8), o[3]);
+                    }
+                    if (gy) {
+                        publish(gy + (int64_t)s * QW, o[1]);
+                        publish(gy + (int64_t)s * QW + 1, o[3]);
+                    }
+                    if (gz) {
+                        publish(gz + (int64_t)s * QW, o[2]);
+                        publish(gz + (int64_t)s * QW + 1, o[3]);
+                    }
                 }
-                q_jitter(X, tile, s, t);
-                if (yout) {
-                    q_st_remote(yout + (unsigned)(s * QW * 8), o[1]);
-                    q_st_remote(yout + (unsigned)(s * QW * 8 + 8), o[3]);
-                }
-                if (zout) {
-                    q_st_remote(zout + (unsigned)(s * QW * 8), o[2]);
-                    q_st_remote(zout + (unsigned)(s * QW * 8 + 8), o[3]);
-                }
-                if (gy) {
-                    publish(gy + (int64_t)s * QW, o[1]);
-                    publish(gy + (int64_t)s * QW + 1, o[3]);
-                }
-                if (gz) {
-                    publish(gz + (int64_t)s * QW, o[2]);
-                    publish(gz + (int64_t)s * QW + 1, o[3]);
+                if (!(X & 2)) {
+                    double *d = dstL + (int64_t)((lo >> 2) + g) * TS * 4;
+#pragma unroll
+                    for (int L = 0; L < 4; L++) {
+                        __stcg(reinterpret_cast<double2 *>(d + PQ(L) * QP * 4), make_double2(O[L][0], O[L][1]));
+                        __stcg(reinterpret_cast<double2 *>(d + PQ(L) * QP * 4 + 2), make_double2(O[L][2], O[L][3]));
+                    }
                 }
             }
         }
@@ -486,7 +547,9 @@ WaveGeom quad_geom(const int lo[3], const int hi[3]) {
     g.TC = (g.TC + cz - 1) / cz * cz;
     g.ispan = hi[0] - lo[0] + 1;
     g.ispan_pad = (g.ispan + 1) & ~1;
-    g.nsteps = g.ispan + 2 * (QT - 1);
+    // a multiple of 4: the 4-step groups of the lane layout align with the
+    // operand chunks in both sweep directions (chunks hold 8 or 4 steps)
+    g.nsteps = (g.ispan + 2 * (QT - 1) + 3) / 4 * 4;
     g.quad = QT;
     return g;
 }
@@ -573,7 +636,9 @@ static cudaError_t launch_quad_c(const LaneArgs &A, cudaStream_t st) {
     if (A.geom.quad == 16) {
         switch (quad_chunks()) {
             case 204: return launch_quad_k<REV, 16, CY, CZ, 2, 4>(A, st);
-            default: return launch_quad_k<REV, 16, CY, CZ, 2, 3>(A, st);
+            default:
+                return A.hw == 2 ? launch_quad_k<REV, 16, CY, CZ, 2, 3, 1, 2>(A, st)
+                                 : launch_quad_k<REV, 16, CY, CZ, 2, 3, 1, 1>(A, st);
         }
     }
     switch (quad_chunks()) {  // QT = 8: 2 KB of operands per array and step
@@ -629,7 +694,8 @@ bool mic_quad_supported(int nsteps) {
     // the default shape / chunking of each tile edge (what launch_quad_c picks)
     if (quad_threads() == 8 && key == 404 && (quad_chunks() == 0 || quad_chunks() == 802))
         return hw_default() == 2 ? quad_fits<8, 4, 4, 8, 2, 2>(nsteps) : quad_fits<8, 4, 4, 8, 2, 1>(nsteps);
-    if (quad_threads() == 16 && key == 204) return quad_fits<16, 2, 4, 2, 3>(nsteps);
+    if (quad_threads() == 16 && key == 204)
+        return hw_default() == 2 ? quad_fits<16, 2, 4, 2, 3, 2>(nsteps) : quad_fits<16, 2, 4, 2, 3, 1>(nsteps);
     return cy * cz <= 16;  // other (experimental) shapes: the launch reports misfits
 }
 
