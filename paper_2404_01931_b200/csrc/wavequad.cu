@@ -642,8 +642,8 @@ static cudaError_t launch_quad_c(const LaneArgs &A, cudaStream_t st) {
         }
     }
     switch (quad_chunks()) {  // QT = 8: 2 KB of operands per array and step
-        case 403: return launch_quad_k<REV, 8, CY, CZ, 4, 3>(A, st);
-        case 404: return launch_quad_k<REV, 8, CY, CZ, 4, 4>(A, st);
+        case 403: return A.hw == 2 ? launch_quad_k<REV, 8, CY, CZ, 4, 3, 1, 2>(A, st) : launch_quad_k<REV, 8, CY, CZ, 4, 3>(A, st);
+        case 404: return A.hw == 2 ? launch_quad_k<REV, 8, CY, CZ, 4, 4, 1, 2>(A, st) : launch_quad_k<REV, 8, CY, CZ, 4, 4>(A, st);
         case 803: return launch_quad_k<REV, 8, CY, CZ, 8, 3>(A, st);
         case 1602: return launch_quad_k<REV, 8, CY, CZ, 16, 2>(A, st);
         default:
