@@ -162,6 +162,7 @@ struct LaneArgs {
     int prepped = 0;            // quad: halo + ticket already reset (by k_pcg_update)
     int pf = 1;                 // quad: face values loaded ahead by the helper warp
     int hw = 1;                 // quad: helper warps (2: one per face)
+    int lag = 0;                // quad: extra start lag behind cross-cluster producers
     int trace_t0 = 0;           // quad trace: first of the 8 tiles with per-step stamps
     // probe (quad): per-launch [first CTA start, last CTA end] %globaltimer
     // stamps, starts at ts[slot], ends at ts[kProbeSlots + slot], slot =

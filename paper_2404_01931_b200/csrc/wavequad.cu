@@ -279,6 +279,13 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
         auto peek_z = [&](int sp) { return inz ? ld_relaxed(inz + (int64_t)sp * QW) : q_peek(lz_ring + sp * QW); };
         auto spin_z = [&](int sp) { return inz ? q_spin_gpu(inz + (int64_t)sp * QW) : q_poll(lz_ring + sp * QW); };
         const bool fy = iny || ly_ring, fz = inz || lz_ring;
+        // lag (FLIPB200_QUAD_LAG, cross-cluster faces only): start only once
+        // the producer is LAG steps further ahead than the skew requires, so
+        // the face loads of later steps rarely find a pending slot
+        if (A.lag > 0) {
+            if (iny && DY + A.lag < nsteps) (void)spin_y(DY + A.lag);
+            if (inz && DZ + A.lag < nsteps) (void)spin_z(DZ + A.lag);
+        }
         if (fy) sq[1][y_q][y_row][y_col] = DY < nsteps ? spin_y(DY) : nz0;
         if (fz) sq[1][z_q][z_row][z_col] = DZ < nsteps ? spin_z(DZ) : nz0;
         // Face values of the next PF steps are loaded ahead: a global-halo
@@ -668,6 +675,8 @@ cudaError_t launch_mic_quad(bool rev, const LaneArgs &A0, cudaStream_t st) {
     }();
     A.pf = pf;
     A.hw = hw_default();
+    static const int lag = getenv("FLIPB200_QUAD_LAG") ? atoi(getenv("FLIPB200_QUAD_LAG")) : 0;
+    A.lag = lag;
     static const int t0 = getenv("FLIPB200_TRACE_TILE0") ? atoi(getenv("FLIPB200_TRACE_TILE0")) : 0;
     A.trace_t0 = t0;
     int cy, cz;
