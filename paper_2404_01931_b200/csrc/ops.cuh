@@ -32,6 +32,8 @@ struct DevScalars {
     int row_lo[3], row_hi[3];           // bounding box of the pressure rows
     int pad;
     unsigned upd_ticket;                // k_pcg_update's last-block ticket (re-armed to 0)
+    int x_it;                           // last iteration whose x += alpha s k_pcg_dir applied
+    unsigned dir_ticket;                // k_pcg_dir's last-block ticket (re-armed to 0)
 };
 
 // CUDA-event bracketing of one kernel class (bench roofline evidence).

@@ -1154,6 +1154,7 @@ __global__ void k_solve_init(DevScalars *sc, double tol, int64_t n, int relax) {
     double rhsmax = __longlong_as_double((long long)sc->rhsmax_bits);
     sc->target = tol * (rhsmax > 1.0 ? rhsmax : 1.0);  // pressure.py:191-193
     sc->iter = 0;
+    sc->x_it = 0;
     sc->done = 0;
     sc->converged = 0;
     sc->status = 0;
@@ -1209,13 +1210,13 @@ __device__ __forceinline__ void iter_check_body(DevScalars *sc, int64_t max_iter
     }
 }
 
-// x += alpha s; r -= alpha q; max|r| (pressure.py:321-326), four rows in
-// flight per thread; one max per block, and the block that finishes last
-// runs the convergence test (k_iter_check's body), so the PCG loop needs no
-// separate check launch.
+// r -= alpha q; max|r| (pressure.py:323-326), four rows in flight per
+// thread; one max per block, and the block that finishes last runs the
+// convergence test (k_iter_check's body), so the PCG loop needs no separate
+// check launch.  x += alpha s (pressure.py:322) is applied by k_pcg_dir,
+// which reads s anyway (one pass over s per iteration instead of two).
 __global__ void __launch_bounds__(256)
-k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
-             const double *__restrict__ s, const double *__restrict__ q, DevScalars *sc,
+k_pcg_update(int64_t n, double *__restrict__ r, const double *__restrict__ q, DevScalars *sc,
              double *__restrict__ rL, const int *__restrict__ posL, int64_t max_iters,
              double *history, int check, HaloReset H) {
     pdl_wait();
@@ -1228,13 +1229,11 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
     double m = 0.0;
     int64_t i = gtid();
     for (; i + 3 * stride < n; i += 4 * stride) {
-        double xs[4], ss[4], rs[4], qs[4];
+        double rs[4], qs[4];
         int ps[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             const int64_t j = i + u * stride;
-            xs[u] = x[j];
-            ss[u] = s[j];
             rs[u] = r[j];
             qs[u] = q[j];
             ps[u] = rL ? posL[j] : 0;
@@ -1242,7 +1241,6 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             const int64_t j = i + u * stride;
-            x[j] = xs[u] + alpha * ss[u];
             const double ri = rs[u] - alpha * qs[u];
             r[j] = ri;
             if (rL) rL[ps[u]] = ri;
@@ -1250,7 +1248,6 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
         }
     }
     for (; i < n; i += stride) {
-        x[i] = x[i] + alpha * s[i];
         const double ri = r[i] - alpha * q[i];
         r[i] = ri;
         if (rL) rL[posL[i]] = ri;
@@ -1292,13 +1289,35 @@ __global__ void k_inv_diag(int64_t n, const double *__restrict__ diag, double sc
     for (int64_t i = gtid(); i < n; i += gstride()) pc[i] = 1.0 / (scale * diag[i]);
 }
 
-// s = z + beta s (pressure.py:329)
-__global__ void k_pcg_dir(int64_t n, double *__restrict__ s, const double *__restrict__ z,
-                          const DevScalars *sc) {
+// x += alpha s (pressure.py:322) for the iteration whose update ran, and,
+// unless that update ended the solve, s = z + beta s (pressure.py:329).
+// The x step belongs to the iteration k_pcg_update last advanced (sc->iter);
+// sc->x_it records the last one applied, so launches past the end of the
+// solve (or after a breakdown, whose update never ran) change nothing.  Every
+// block reads the flags before the last block (ticket) advances x_it.
+__global__ void __launch_bounds__(256)
+k_pcg_dir(int64_t n, double *__restrict__ s, const double *__restrict__ z,
+          double *__restrict__ x, DevScalars *sc) {
     pdl_wait();
-    if (sc->done) return;
-    double beta = sc->beta;
-    for (int64_t i = gtid(); i < n; i += gstride()) s[i] = z[i] + beta * s[i];
+    const int it = sc->iter;
+    if (it <= sc->x_it) return;  // this iteration's update did not run
+    const bool dir = !sc->done;
+    const double alpha = sc->alpha, beta = sc->beta;
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        const double si = s[i];
+        x[i] = x[i] + alpha * si;
+        if (dir) s[i] = z[i] + beta * si;
+    }
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&sc->dir_ticket, 1u) == gridDim.x - 1;
+        if (last) {
+            sc->dir_ticket = 0u;
+            sc->x_it = it;
+        }
+    }
 }
 
 __global__ void k_fill(double *a, int64_t n, double v) {
@@ -1647,8 +1666,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 (*launches)++;
             }
             launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
-                       B.x + o, B.r + o, (const double *)(B.s + o),
-                       (const double *)(B.q + o), sc,
+                       B.r + o, (const double *)(B.q + o), sc,
                        (lane && !sl) ? LV.lane->rL : nullptr,
                        (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
                        (int64_t)cfg.max_iters, cfg.history, sl ? 0 : 1,
@@ -1666,7 +1684,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 solver_dot(cfg, LdProd{B.z, B.r}, nf, B.dot_tmp, EPI_SIGMA_NEW, sc, st,
                            launches);
             launch_pdl(k_pcg_dir, wave_blocks(k_pcg_dir, n), kThreads, 0, st, n, B.s + o,
-                       (const double *)(B.z + o), (const DevScalars *)sc);
+                       (const double *)(B.z + o), B.x + o, sc);
             if (sl) slab_halo(cfg, B.s);
             *launches += 2;  // update (with the convergence test) + dir
         } else {  // pressure.py:209-213
