@@ -1540,6 +1540,31 @@ static void apply_pc(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     }
 }
 
+// Inputs of the quad MIC(0) build in the lane layout: diag, and per row the
+// code k_x + 3 k_y + 9 k_z, k_p = how many of the pair-p lower neighbour's
+// o1 / o2 neighbours are rows (_core.pyx:285-303).  Only row entries are
+// written (the others keep the ABSENT marker k_lane_map put there).
+__global__ void k_build_inputs(SysView S, const int *__restrict__ posL, double *__restrict__ diagL,
+                               double *__restrict__ codeL) {
+    const int dprev[3] = {0, 2, 4}, o1[3] = {3, 1, 1}, o2[3] = {5, 5, 3};
+    const int *nb = S.nbr;
+    const int64_t ld = S.ldn;
+    for (int64_t r = gtid(); r < S.n; r += gstride()) {
+        int code = 0, mul = 1;
+#pragma unroll
+        for (int p = 0; p < 3; p++) {
+            const int q = nb[dprev[p] * ld + r];
+            int k = 0;
+            if (q >= 0) k = (nb[o1[p] * ld + q] >= 0) + (nb[o2[p] * ld + q] >= 0);
+            code += k * mul;
+            mul *= 3;
+        }
+        const int e = posL[r];
+        diagL[e] = S.diag[r];
+        codeL[e] = (double)code;
+    }
+}
+
 // Device-driven solver loop: a graph holding one WHILE conditional node
 // whose body (captured from the stream) is one solver iteration followed by
 // k_loop_cond, which keeps the loop running while the done flag is clear.
@@ -1623,11 +1648,39 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     const bool lane = cfg.precond == FLIP_PRECOND_MIC0 && LV.lane;
     if (nf > 0 && !relax) {
         if (cfg.precond == FLIP_PRECOND_MIC0) {
-            do_sweep<SW_MIC_BUILD>(sl ? *cfg.full : S, LV, nullptr, B.precon, nullptr, sc, st,
-                                   launches);
-            if (LV.lane) {
-                launch_rows_to_lane(B.precon, LV.lane->posL, nf, LV.lane->preL, sc, st);
-                (*launches)++;
+            // quad lane path: the build runs on the quad wavefront too
+            // (inputs in the lane layout, precon straight into it); 0.56 ms
+            // on the row-layout wavefront at 256^3
+            static const bool qbuild = !getenv("FLIPB200_QUAD_BUILD") || atoi(getenv("FLIPB200_QUAD_BUILD"));
+            bool built = false;
+            if (LV.lane && LV.lane->hr.on && qbuild) {
+                const SysView &F = sl ? *cfg.full : S;
+                const LaneBufs &Lb = *LV.lane;
+                k_build_inputs<<<nblocks(F.n), kThreads, 0, st>>>(F, Lb.posL, Lb.rL, Lb.tqL);
+                LaneArgs A = Lb.args;
+                A.src = Lb.rL;
+                A.precon = Lb.tqL;
+                A.dst = Lb.preL;
+                A.sc = nullptr;
+                A.halo_y = Lb.hr.hy[0];
+                A.ticket = Lb.hr.ticket[0];
+                const cudaError_t e = launch_mic_lane_build(A, st);
+                if (e == cudaSuccess) {
+                    // the row-order copy (slab gathers, debug reads)
+                    launch_lane_to_rows(Lb.preL, Lb.posL, nf, B.precon, nullptr, st);
+                    *launches += 4;
+                    built = true;
+                } else {
+                    cudaGetLastError();
+                }
+            }
+            if (!built) {
+                do_sweep<SW_MIC_BUILD>(sl ? *cfg.full : S, LV, nullptr, B.precon, nullptr, sc, st,
+                                       launches);
+                if (LV.lane) {
+                    launch_rows_to_lane(B.precon, LV.lane->posL, nf, LV.lane->preL, sc, st);
+                    (*launches)++;
+                }
             }
         }
         else if (cfg.precond == FLIP_PRECOND_JACOBI) {

@@ -1123,6 +1123,23 @@ static cudaError_t launch_lane_shape(const LaneArgs &A, cudaStream_t st) {
     return cudaPeekAtLastError();
 }
 
+// MIC(0) build on the quad wavefront (launch_mic_quad_build), after the
+// forward direction's halo reset (as launch_mic_lane does for a sweep).
+cudaError_t launch_mic_lane_build(const LaneArgs &A, cudaStream_t st) {
+    if (!A.geom.quad) return cudaErrorNotSupported;
+    const int64_t tiles = (int64_t)A.geom.TB * A.geom.TC;
+    int cy = 0, cz = 0;
+    quad_cluster_shape(&cy, &cz);
+    const int QW = A.geom.ty;
+    const int64_t nsel = (int64_t)(A.geom.TB / cy) * A.geom.TC * A.geom.nsteps * QW +
+                         (int64_t)A.geom.TB * (A.geom.TC / cz) * A.geom.nsteps * QW;
+    LaneArgs B = A;
+    B.halo_z = A.halo_y + tiles * A.geom.nsteps * QW;
+    launch_pdl(k_wave_prep_cl, nblocks(nsel), kThreads, 0, st, A.halo_y, B.halo_z, A.geom.TB,
+               A.geom.TC, A.geom.nsteps, QW, QW, cy, cz, 0, A.ticket, (const DevScalars *)nullptr);
+    return launch_mic_quad_build(B, st);
+}
+
 cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st) {
     if (A.geom.quad) {
         // cross-cluster faces only (as k_wave_prep_cl for k_mic_cl), 32 wide

@@ -218,10 +218,12 @@ bool mic_quad_supported(int nsteps);
 int quad_cluster_shape(int *cy, int *cz);
 WaveGeom quad_geom(const int lo[3], const int hi[3]);
 cudaError_t launch_mic_quad(bool rev, const LaneArgs &A, cudaStream_t st);
+cudaError_t launch_mic_quad_build(const LaneArgs &A, cudaStream_t st);
 __global__ void k_wave_prep_cl(double *halo_y, double *halo_z, int TB, int TC, int nsteps, int ty,
                                int tz, int cy, int cz, int rev, int *ticket, const DevScalars *sc);
 __global__ void k_wave_prep(double *halo, int64_t nh, int *ticket, const DevScalars *sc);
 cudaError_t launch_mic_lane(bool rev, const LaneArgs &A, cudaStream_t st);
+cudaError_t launch_mic_lane_build(const LaneArgs &A, cudaStream_t st);
 // wavecl.cu: cluster/DSMEM variant (FLIPB200_CLUSTER=CYxCZ); NotSupported if off
 cudaError_t launch_mic_cluster(bool rev, const LaneArgs &A, cudaStream_t st);
 int mic_cluster_pad(int *cy, int *cz);

@@ -153,9 +153,39 @@ __device__ __forceinline__ double mic_cell_v(double a, double pr, double pv, dou
     return row ? o : -0.0;
 }
 
+// One cell of the MIC(0) build (_core.pyx:291-307), the forward
+// recurrence that produces precon.  a = diag (ABSENT off the rows), code =
+// k_x + 3 k_y + 9 k_z with k_p the number of the lower neighbour's two
+// "other" neighbours that are rows (o1/o2 of the pair), pv / yv / zv = the
+// precon of the -x / -y / -z neighbour, or +-0.0 when that neighbour is not
+// a row: with pq == 0 both updates of its pair subtract a zero, an exact
+// no-op, as the reference's skipped pair (precon itself is never 0).
+__device__ __forceinline__ double mic_build_v(double diag, double code, double pv, double yv,
+                                              double zv, double scale, bool row, double &stored) {
+    const double absent = __longlong_as_double((long long)WAVE_ABSENT);
+    const double tau = 0.97, sigma = 0.25;  // mic0_build's defaults (_core.pyx:275-276)
+    const int cd = row ? (int)code : 0;
+    double e = diag * scale;
+    const double pq3[3] = {pv, yv, zv};
+    const int kp[3] = {cd % 3, (cd / 3) % 3, cd / 9};
+#pragma unroll
+    for (int p = 0; p < 3; p++) {
+        const double pq = pq3[p];
+        e = e - (scale * pq) * (scale * pq);
+        double others = 0.0;
+        if (kp[p] > 0) others = others - scale;
+        if (kp[p] > 1) others = others - scale;
+        e = e - (((tau * (-scale)) * others) * pq) * pq;
+    }
+    if (e < (sigma * diag) * scale) e = diag * scale;
+    const double o = 1.0 / sqrt(e);
+    stored = row ? o : absent;
+    return row ? o : -0.0;
+}
+
 // QT threads per tile edge (16 or 8): a tile is 2QT x 2QT pencils, the
 // faces are QW = 2QT values wide.
-template <bool REV, int QT, int CY, int CZ, int KC, int NB, int PF, int HW = 1>
+template <bool REV, int QT, int CY, int CZ, int KC, int NB, int PF, int HW = 1, int BUILD = 0>
 __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
     constexpr int QP = QT * QT, QW = 2 * QT;
     constexpr int DY = QT - 1, DZ = QT - 1;
@@ -436,10 +466,17 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
                         asm volatile("" ::: "memory");
                     }
                     double o[4];
-                    o[0] = mic_cell_v<REV>(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), O[0][w]);
-                    o[1] = mic_cell_v<REV>(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), O[1][w]);
-                    o[2] = mic_cell_v<REV>(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), O[2][w]);
-                    o[3] = mic_cell_v<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), O[3][w]);
+                    if (BUILD) {
+                        o[0] = mic_build_v(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), O[0][w]);
+                        o[1] = mic_build_v(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), O[1][w]);
+                        o[2] = mic_build_v(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), O[2][w]);
+                        o[3] = mic_build_v(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), O[3][w]);
+                    } else {
+                        o[0] = mic_cell_v<REV>(a[0], pr[0], pv[0], y0, z0, sc, valid[0] && present(a[0]), O[0][w]);
+                        o[1] = mic_cell_v<REV>(a[1], pr[1], pv[1], o[0], z1, sc, valid[1] && present(a[1]), O[1][w]);
+                        o[2] = mic_cell_v<REV>(a[2], pr[2], pv[2], y2, o[0], sc, valid[2] && present(a[2]), O[2][w]);
+                        o[3] = mic_cell_v<REV>(a[3], pr[3], pv[3], o[2], o[1], sc, valid[3] && present(a[3]), O[3][w]);
+                    }
 #pragma unroll
                     for (int L = 0; L < 4; L++) {
                         sq[cur][PQ(L)][kk + 1][jj + 1] = o[L];
@@ -561,7 +598,7 @@ WaveGeom quad_geom(const int lo[3], const int hi[3]) {
     return g;
 }
 
-template <bool REV, int QT, int CY, int CZ, int KC, int NB, int PF = 1, int HW = 1>
+template <bool REV, int QT, int CY, int CZ, int KC, int NB, int PF = 1, int HW = 1, int BUILD = 0>
 static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     constexpr int QP = QT * QT, QW = 2 * QT;
     const int tiles = A.geom.TB * A.geom.TC;
@@ -569,11 +606,11 @@ static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     static const size_t pad = getenv("FLIPB200_QUAD_PAD") ? (size_t)atoi(getenv("FLIPB200_QUAD_PAD")) * 1024 : 0;
     const size_t smem = rings + (size_t)NB * 2 * KC * 4 * QP * sizeof(double) + pad;
     static cudaError_t attr = [] {
-        cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW>,
+        cudaError_t e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW, BUILD>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024 - 24 * 1024);
         if (e == cudaSuccess && CY * CZ > 8)
-            e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW>,
+            e = cudaFuncSetAttribute(k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW, BUILD>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         return e;
     }();
@@ -593,7 +630,7 @@ static cudaError_t launch_quad_k(const LaneArgs &A, cudaStream_t st) {
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW>, A);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_mic_quad<REV, QT, CY, CZ, KC, NB, PF, HW, BUILD>, A);
     return e != cudaSuccess ? e : cudaPeekAtLastError();
 }
 
@@ -694,6 +731,24 @@ cudaError_t launch_mic_quad(bool rev, const LaneArgs &A0, cudaStream_t st) {
     QCASE(4, 8)
 #undef QCASE
     return cudaErrorNotSupported;
+}
+
+// The MIC(0) build on the quad wavefront (forward order): A.src = diag and
+// A.precon = pair codes in the lane layout, A.dst = precon (lane layout).
+// Only the default shape (8 x 8 threads, 4 x 4 clusters, 8-step chunks).
+cudaError_t launch_mic_quad_build(const LaneArgs &A0, cudaStream_t st) {
+    LaneArgs A = A0;
+    A.dbg = 0;
+    A.pf = 1;
+    A.hw = hw_default();
+    A.trace = nullptr;
+    A.ts = nullptr;
+    int cy, cz;
+    quad_cluster_shape(&cy, &cz);
+    if (A.geom.quad != 8 || cy != 4 || cz != 4 || quad_chunks() != 0 || A.geom.TB % 4 || A.geom.TC % 4)
+        return cudaErrorNotSupported;
+    return A.hw == 2 ? launch_quad_k<false, 8, 4, 4, 8, 2, 1, 2, 1>(A, st)
+                     : launch_quad_k<false, 8, 4, 4, 8, 2, 1, 1, 1>(A, st);
 }
 
 bool mic_quad_supported(int nsteps) {
