@@ -11,7 +11,10 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libflipb200.so")
+# FLIPB200_CHECKED=1: the bounds-checked build (FLIP_CHECK sites trap on an
+# out-of-range index; `make -C paper_2404_01931_b200/csrc checked`)
+LIB_PATH = os.path.join(HERE, "libflipb200_checked.so" if os.environ.get("FLIPB200_CHECKED") == "1"
+                        else "libflipb200.so")
 
 FLIP_OK = 0
 FLIP_E_CONFIG = 1

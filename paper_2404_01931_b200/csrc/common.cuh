@@ -10,6 +10,7 @@
 //      pairwise tree; order-free ones (max, integer counts) use atomics.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include "../../include/flipb200.h"
@@ -21,6 +22,27 @@
 #define MAX_PER_CELL 12  // flipsim/particles.py:152
 
 namespace flip {
+
+// Bounds checks of the checked build (make checked -> libflipb200_checked.so,
+// loaded with FLIPB200_CHECKED=1): a failed check prints the site and the
+// offending value and traps, which fails the launch (compute-sanitizer is
+// not available on the GPU pool).  Compiled out of the production library.
+#ifdef FLIP_CHECKED
+#define FLIP_CHECK(cond, what, v, lim)                                                       \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("FLIP_CHECK failed: %s (%lld vs %lld) at %s:%d block %d thread %d\n", \
+                   what, (long long)(v), (long long)(lim), __FILE__, __LINE__,          \
+                   (int)blockIdx.x, (int)threadIdx.x);                                 \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define FLIP_CHECK(cond, what, v, lim) \
+    do {                               \
+    } while (0)
+#endif
+#define FLIP_CHECK_RANGE(i, n, what) FLIP_CHECK((i) >= 0 && (i) < (n), what, i, n)
 
 constexpr int kThreads = 256;
 

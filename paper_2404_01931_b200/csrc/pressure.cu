@@ -925,7 +925,9 @@ struct LdLaneDot {
     const int *posL;
     double *z;
     const double *r;
+    int64_t nL = INT64_MAX;  // lane-layout entries (checked build)
     __device__ __forceinline__ double operator()(int64_t i) const {
+        FLIP_CHECK_RANGE((int64_t)posL[i], nL, "z.r dot lane gather");
         double zi = zL[posL[i]];
         z[i] = zi;
         return zi * r[i];
@@ -1237,6 +1239,7 @@ k_pcg_update(int64_t n, double *__restrict__ r, const double *__restrict__ q, De
             rs[u] = r[j];
             qs[u] = q[j];
             ps[u] = rL ? posL[j] : 0;
+            if (rL && H.on) FLIP_CHECK_RANGE(ps[u], (int64_t)H.TB * H.TC * H.nsteps * H.W * H.W, "update r scatter");
         }
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -1731,7 +1734,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             }
             apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
             if (lane)
-                solver_dot(cfg, LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r}, nf, B.dot_tmp,
+                solver_dot(cfg, LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r, lane_entries(LV.lane->args.geom)}, nf, B.dot_tmp,
                            EPI_SIGMA_NEW, sc, st, launches);
             else
                 solver_dot(cfg, LdProd{B.z, B.r}, nf, B.dot_tmp, EPI_SIGMA_NEW, sc, st,

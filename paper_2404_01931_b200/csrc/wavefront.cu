@@ -861,6 +861,7 @@ __global__ void k_lane_map(WaveGeom G, Dims d, int TY, int TZ, const uint8_t *__
             if (isrow[cell]) row = rowscan[cell];
         }
         lrow[e] = row;
+        FLIP_CHECK(e < (int64_t)INT_MAX, "lane entry index", e, INT_MAX);
         if (row >= 0) posL[row] = (int)e;
         absent1[e] = ab;
         absent2[e] = ab;

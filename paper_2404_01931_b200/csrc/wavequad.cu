@@ -212,6 +212,11 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
     }
     const WaveGeom G = A.geom;
     const int nsteps = G.nsteps;
+    // lane-layout entries and halo words per direction (checked build)
+    const int64_t lane_n = (int64_t)G.TB * G.TC * nsteps * 4 * QP;
+    const int64_t halo_n = (int64_t)G.TB * G.TC * nsteps * QW;
+    (void)lane_n;
+    (void)halo_n;
     double *yring = ring, *zring = ring + (int64_t)nsteps * QW;
     const unsigned cr = q_rank();
     const int ry = (int)cr / CZ, rz = (int)cr % CZ;
@@ -226,6 +231,7 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
     }
     q_cluster_sync();
     const int tk = cr == 0 ? s_tile : q_ld_remote_int(q_map(&s_tile, 0));
+    FLIP_CHECK_RANGE(tk, (int)(gridDim.x / (CY * CZ)), "quad cluster ticket");
     int bq, cq;
     q_cluster_tile(tk, G.TB / CY, G.TC / CZ, bq, cq);
     int b = bq * CY + ry, c = cq * CZ + rz;
@@ -255,6 +261,8 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
         const int buf = ch % NB;
         const unsigned bytes = (unsigned)(cnt * TS * 8);
         mbar_expect_tx(&mbar[buf], 2 * bytes);
+        FLIP_CHECK(lo >= 0 && lo + cnt <= nsteps && cnt % 4 == 0, "quad chunk", lo, nsteps);
+        FLIP_CHECK_RANGE(tbase + (int64_t)(lo + cnt) * TS - 1, lane_n, "quad chunk source");
         bulk_g2s(opb + (buf * 2 + 0) * KC * TS, A.src + tbase + (int64_t)lo * TS, bytes, &mbar[buf]);
         bulk_g2s(opb + (buf * 2 + 1) * KC * TS, A.precon + tbase + (int64_t)lo * TS, bytes,
                  &mbar[buf]);
@@ -304,9 +312,17 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
         if (l == 0 && hw == 0)
             for (int q = 0; q < NB; q++) issue(q);
         // slot of producer step sp: global halo or local DSMEM ring
-        auto peek_y = [&](int sp) { return iny ? ld_relaxed(iny + (int64_t)sp * QW) : q_peek(ly_ring + sp * QW); };
+        auto peek_y = [&](int sp) {
+            FLIP_CHECK_RANGE(sp, nsteps, "quad y face slot");
+            if (iny) FLIP_CHECK_RANGE(iny + (int64_t)sp * QW - A.halo_y, halo_n, "quad y halo read");
+            return iny ? ld_relaxed(iny + (int64_t)sp * QW) : q_peek(ly_ring + sp * QW);
+        };
         auto spin_y = [&](int sp) { return iny ? q_spin_gpu(iny + (int64_t)sp * QW) : q_poll(ly_ring + sp * QW); };
-        auto peek_z = [&](int sp) { return inz ? ld_relaxed(inz + (int64_t)sp * QW) : q_peek(lz_ring + sp * QW); };
+        auto peek_z = [&](int sp) {
+            FLIP_CHECK_RANGE(sp, nsteps, "quad z face slot");
+            if (inz) FLIP_CHECK_RANGE(inz + (int64_t)sp * QW - A.halo_z, halo_n, "quad z halo read");
+            return inz ? ld_relaxed(inz + (int64_t)sp * QW) : q_peek(lz_ring + sp * QW);
+        };
         auto spin_z = [&](int sp) { return inz ? q_spin_gpu(inz + (int64_t)sp * QW) : q_poll(lz_ring + sp * QW); };
         const bool fy = iny || ly_ring, fz = inz || lz_ring;
         // lag (FLIPB200_QUAD_LAG, cross-cluster faces only): start only once
@@ -484,6 +500,7 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
                     }
                     q_jitter(X, tile, s, t);
                     if (yout) {
+                        FLIP_CHECK_RANGE(s, nsteps, "quad y DSMEM ring");
                         q_st_remote(yout + (unsigned)(s * QW * 8), o[1]);
                         q_st_remote(yout + (unsigned)(s * QW * 8 + 8), o[3]);
                     }
@@ -492,16 +509,19 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
                         q_st_remote(zout + (unsigned)(s * QW * 8 + 8), o[3]);
                     }
                     if (gy) {
+                        FLIP_CHECK_RANGE(gy + (int64_t)s * QW + 1 - A.halo_y, halo_n, "quad y halo publish");
                         publish(gy + (int64_t)s * QW, o[1]);
                         publish(gy + (int64_t)s * QW + 1, o[3]);
                     }
                     if (gz) {
+                        FLIP_CHECK_RANGE(gz + (int64_t)s * QW + 1 - A.halo_z, halo_n, "quad z halo publish");
                         publish(gz + (int64_t)s * QW, o[2]);
                         publish(gz + (int64_t)s * QW + 1, o[3]);
                     }
                 }
                 if (!(X & 2)) {
                     double *d = dstL + (int64_t)((lo >> 2) + g) * TS * 4;
+                    FLIP_CHECK_RANGE(d + PQ(3) * QP * 4 + 3 - A.dst, lane_n, "quad group store");
 #pragma unroll
                     for (int L = 0; L < 4; L++) {
                         __stcg(reinterpret_cast<double2 *>(d + PQ(L) * QP * 4), make_double2(O[L][0], O[L][1]));
