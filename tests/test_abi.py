@@ -24,6 +24,17 @@ def test_library_exports_every_header_symbol(pkg):
     assert len(header_symbols()) >= 30
 
 
+def test_checked_library_exports_the_same_symbols(pkg):
+    """The bounds-checked variant (FLIPB200_CHECKED=1) is a drop-in copy of the ABI."""
+    path = os.path.join(ROOT, "paper_2404_01931_b200", "libflipb200_checked.so")
+    if not os.path.exists(path):
+        pytest.skip("checked library not built (make -C paper_2404_01931_b200/csrc checked)")
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\bT (flip_[a-z0-9_]+)", out))
+    assert not [s for s in header_symbols() if s not in exported]
+
+
 def test_ctypes_binds_every_header_symbol(pkg):
     from paper_2404_01931_b200 import _lib
     for s in header_symbols():
