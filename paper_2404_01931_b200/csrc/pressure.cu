@@ -1280,6 +1280,64 @@ __global__ void k_iter_check(DevScalars *sc, int64_t max_iters, double *history)
     iter_check_body(sc, max_iters, history, __longlong_as_double((long long)sc->res_bits));
 }
 
+// Jacobi on the compact stencil (_core.pyx:216-234): the neighbour sum in
+// nbr order, (rhs / scale + s) / diag with diag the exact neighbour count.
+__device__ __forceinline__ double compact_sum(const SysView &S, const double *__restrict__ x,
+                                              int64_t r, unsigned m) {
+    const unsigned d = S.dy[r];
+    const int2 z = S.dz[r];
+    double s = 0.0;
+    if (m & 1u) s = s + x[r - 1];
+    if (m & 2u) s = s + x[r + 1];
+    if (m & 4u) s = s + x[r - (int64_t)(d & 0xffffu)];
+    if (m & 8u) s = s + x[r + (int64_t)(d >> 16)];
+    if (m & 16u) s = s + x[r - (int64_t)z.x];
+    if (m & 32u) s = s + x[r + (int64_t)z.y];
+    return s;
+}
+
+__global__ void __launch_bounds__(256)
+k_jacobi_c(SysView S, const double *__restrict__ x, double *__restrict__ out, const DevScalars *sc) {
+    pdl_wait();
+    if (sc->done) return;
+    for (int64_t r = S.r0 + gtid(); r < S.r0 + S.n; r += gstride()) {
+        const unsigned m = S.meta[r];
+        out[r] = (S.rhs[r] / S.scale + compact_sum(S, x, r, m)) / (double)(m >> 8);
+    }
+}
+
+// max |rhs - A x| of the new Jacobi iterate (pressure.py:59-62, k_matvec's
+// arithmetic); the block that finishes last runs the convergence test
+// (k_iter_check's body), so an iteration is two launches.
+__global__ void __launch_bounds__(256)
+k_resid_c(SysView S, const double *__restrict__ x, DevScalars *sc, int64_t max_iters,
+          double *history) {
+    pdl_wait();
+    if (sc->done) return;
+    __shared__ double wm[8];
+    __shared__ bool last;
+    double mx = 0.0;
+    for (int64_t r = S.r0 + gtid(); r < S.r0 + S.n; r += gstride()) {
+        const unsigned m = S.meta[r];
+        const double yr = S.scale * ((double)(m >> 8) * x[r] - compact_sum(S, x, r, m));
+        mx = fmax(mx, fabs(S.rhs[r] - yr));
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) mx = fmax(mx, wm[w]);
+        if (mx > 0.0) atomic_max_nonneg(&sc->res_bits, mx);
+        __threadfence();
+        last = atomicAdd(&sc->upd_ticket, 1u) == gridDim.x - 1;
+        if (last) {
+            sc->upd_ticket = 0u;
+            const double res = __longlong_as_double((long long)atomicAdd(&sc->res_bits, 0ull));
+            iter_check_body(sc, max_iters, history, res);
+        }
+    }
+}
+
 // z = r * inv_diag (Jacobi preconditioner, pressure.py:289-293) or z = r
 __global__ void k_precond_diag(int64_t n, const double *__restrict__ r, const double *__restrict__ pc,
                                double *__restrict__ z, const DevScalars *sc, int check_done) {
@@ -1701,6 +1759,11 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
         // gathered rhs (every rank then holds the same full iterate)
         slab_gather_rows(cfg, const_cast<double *>(S.rhs));
     }
+    // Jacobi on the compact stencil with ping-pong iterates and the test in
+    // the residual kernel (one GPU): two PDL launches per iteration
+    static const bool jfast_env = !getenv("FLIPB200_JACOBI_PLAIN");
+    const bool jfast = cfg.solver == FLIP_SOLVER_JACOBI && !sl && S.meta && jfast_env;
+    int64_t jit = 0;  // Jacobi iterations issued (buffer parity)
     // one iteration of SOLVERS[cfg.solver] (pressure.py:209-213 / 314-331)
     auto one_iter = [&]() {
         if (!relax) {  // pressure.py:314-331
@@ -1744,6 +1807,18 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             if (sl) slab_halo(cfg, B.s);
             *launches += 2;  // update (with the convergence test) + dir
         } else {  // pressure.py:209-213
+            if (cfg.solver == FLIP_SOLVER_JACOBI && jfast) {
+                // ping-pong iterates (the reference's x = sweep(x) makes a new
+                // array): iteration k reads buf[(k-1)%2], writes buf[k%2]
+                double *xin = (jit & 1) ? B.xtmp : B.x, *xout = (jit & 1) ? B.x : B.xtmp;
+                jit++;
+                launch_pdl(k_jacobi_c, wave_blocks(k_jacobi_c, n), kThreads, 0, st, S,
+                           (const double *)xin, xout, (const DevScalars *)sc);
+                launch_pdl(k_resid_c, wave_blocks(k_resid_c, n), kThreads, 0, st, S,
+                           (const double *)xout, sc, (int64_t)cfg.max_iters, cfg.history);
+                *launches += 2;
+                return;  // the convergence test ran in k_resid_c
+            }
             if (cfg.solver == FLIP_SOLVER_JACOBI) {
                 k_jacobi<<<nblocks(n), kThreads, 0, st>>>(S, B.x, B.xtmp, sc, 1);
                 if (sl) slab_halo(cfg, B.xtmp);
@@ -1858,6 +1933,9 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     cudaMemcpyAsync(sch, sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
     FLIP_CUDA_OK(cudaStreamSynchronize(st));
     FLIP_CUDA_OK(cudaGetLastError());
+    if (jfast && (sch->iter & 1)) {  // iteration K wrote buf[K % 2]: xtmp for odd K
+        FLIP_CUDA_OK(cudaMemcpyAsync(B.x, B.xtmp, sizeof(double) * nf, cudaMemcpyDeviceToDevice, st));
+    }
     if (graph_per_iter) {  // body executions x (its iterations' kernels + the loop test)
         const int64_t bodies = std::max<int64_t>(1, (sch->iter + graph_unroll - 1) / graph_unroll);
         *launches = graph_l0 + bodies * (graph_unroll * graph_per_iter + 1);
@@ -1955,7 +2033,8 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         S.n = SL.R1 - SL.R0;
     }
     static const bool plain_mv = getenv("FLIPB200_PLAIN_MATVEC") != nullptr;
-    if (prm.solver == FLIP_SOLVER_PCG && n > 0 && c.d.nx < 32768 && !plain_mv) {
+    if ((prm.solver == FLIP_SOLVER_PCG || prm.solver == FLIP_SOLVER_JACOBI) && n > 0 &&
+        c.d.nx < 32768 && !plain_mv) {
         k_compact_nbr<<<nblocks(S.n), kThreads, 0, st>>>(S, c.nb_meta, c.nb_dy, c.nb_dz);
         c.launches++;
         S.meta = c.nb_meta;
