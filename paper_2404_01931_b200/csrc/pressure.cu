@@ -521,7 +521,8 @@ static int pw_cut(int64_t n) {
 int64_t dot_tmp_doubles(int64_t n) {
     int cut = pw_cut(n > 0 ? n : 1);
     int64_t nodes = (int64_t)1 << cut;
-    return 2 * ((nodes + 31) / 32) + 64;
+    // k_dot_fused/k_dot_nodes partials, or k_dot_staged's units (nodes / 8 at most)
+    return std::max<int64_t>(2 * ((nodes + 31) / 32), nodes / 8 + 1) + 64;
 }
 
 // epi/sc select a fused scalar update; for EPI_STORE the sum goes to *out_dev.
@@ -1381,6 +1382,234 @@ k_pcg_dir(int64_t n, double *__restrict__ s, const double *__restrict__ z,
     }
 }
 
+// Pairwise dot with its summands produced row-coalesced (a row per thread,
+// RB rows per thread in flight) into shared memory, then summed there in
+// numpy's order (one GPU).  A unit is npu consecutive cut-level nodes of the
+// tree (k_dot_fused's nodes); its rows [start, end) are produced by the whole
+// block, then each node is summed by an 8-lane group (pw_node8 on the shared
+// copy), the unit's nodes by the perfect tree, and the last block reduces the
+// unit partials (perfect tree) and runs the epilogue.  Units are handed out by
+// an atomic counter.  Same additions in the same order as k_dot_fused, so
+// the same bits; what changes is the access pattern of the producer: a row
+// functor F gets three phases (independent loads, dependent loads, compute +
+// stores) so a thread's RB rows have their loads in flight together.
+struct StagedPlan {
+    int64_t n = -1;
+    int cut = 0, npu = 0;
+    int64_t units = 0, smem = 0;
+    bool ok = false;
+};
+constexpr int kStagedMaxUnits = 4096;  // 16 partials per thread in the last block (2^17 nodes)
+
+__device__ __forceinline__ void pw_node_span(int64_t n, int cut, int64_t node, int64_t *s,
+                                             int64_t *len) {
+    int64_t s0 = 0, l = n;
+    for (int lvl = cut - 1; lvl >= 0; lvl--) {
+        const int64_t n2 = pw_split(l);
+        if ((node >> lvl) & 1) {
+            s0 += n2;
+            l -= n2;
+        } else {
+            l = n2;
+        }
+    }
+    *s = s0;
+    *len = l;
+}
+
+struct LdSmem {
+    const double *p;  // p[i - base] = summand i (base = the unit's first row)
+    int64_t base;
+    __device__ __forceinline__ double operator()(int64_t i) const { return p[(int)(i - base)]; }
+};
+
+// a[i] * b[i] (LdProd), row-coalesced: the s.q dot (pressure.py:316)
+struct RowProd {
+    const double *__restrict__ a;
+    const double *__restrict__ b;
+    struct A { double x, y; };
+    struct B {};
+    __device__ __forceinline__ A pre(int64_t i) const { return {a[i], b[i]}; }
+    __device__ __forceinline__ B mid(int64_t, const A &) const { return {}; }
+    __device__ __forceinline__ double post(int64_t, const A &v, const B &) const { return v.x * v.y; }
+};
+
+// z from the lane-major layout of the MIC(0) sweep (LdLaneDot): z[r] written,
+// summand z[r] * r[r]: pressure.py:328-329.
+struct RowLaneDot {
+    const double *__restrict__ zL;
+    const int *__restrict__ posL;
+    double *__restrict__ z;
+    const double *__restrict__ r;
+    int64_t nL;
+    struct A { int p; double rr; };
+    struct B { double zi; };
+    __device__ __forceinline__ A pre(int64_t i) const { return {posL[i], r[i]}; }
+    __device__ __forceinline__ B mid(int64_t, const A &a) const {
+        FLIP_CHECK_RANGE((int64_t)a.p, nL, "z.r dot lane gather");
+        return {zL[a.p]};
+    }
+    __device__ __forceinline__ double post(int64_t i, const A &a, const B &b) const {
+        z[i] = b.zi;
+        return b.zi * a.rr;
+    }
+};
+
+template <class F, int RB>
+__global__ void __launch_bounds__(256)
+k_dot_staged(F f, int64_t n, int cut, int npu, int64_t units, double *__restrict__ part,
+             unsigned *ctr, int epi, DevScalars *sc) {
+    extern __shared__ double prod[];
+    __shared__ double sv[256];
+    __shared__ int64_t span[2];
+    __shared__ long long unit_s;
+    __shared__ bool last;
+    pdl_wait();
+    if (sc->done) return;  // uniform: the flag changes only in the last block
+    const int tid = threadIdx.x;
+    const int grp = tid >> 3, g = tid & 7;
+    while (true) {
+        if (tid == 0) unit_s = (long long)atomicAdd(&ctr[1], 1u);
+        __syncthreads();
+        const int64_t u = unit_s;
+        if (u >= units) break;
+        int64_t ns = 0, nl = 0;
+        if (grp < npu) {
+            pw_node_span(n, cut, u * npu + grp, &ns, &nl);
+            if (tid == 0) span[0] = ns;
+            if (grp == npu - 1 && g == 0) span[1] = ns + nl;
+        }
+        __syncthreads();
+        const int64_t a0 = span[0], b0 = span[1];
+        for (int64_t rb = a0 + tid; rb < b0; rb += RB * 256) {
+            typename F::A pa[RB];
+            typename F::B pb[RB];
+#pragma unroll
+            for (int k = 0; k < RB; k++)
+                if (rb + k * 256 < b0) pa[k] = f.pre(rb + k * 256);
+#pragma unroll
+            for (int k = 0; k < RB; k++)
+                if (rb + k * 256 < b0) pb[k] = f.mid(rb + k * 256, pa[k]);
+#pragma unroll
+            for (int k = 0; k < RB; k++)
+                if (rb + k * 256 < b0) prod[rb + k * 256 - a0] = f.post(rb + k * 256, pa[k], pb[k]);
+        }
+        __syncthreads();
+        double val = 0.0;
+        if (grp < npu) val = pw_node8<2>(LdSmem{prod, a0}, ns, nl, g);
+        // the unit's perfect tree (pairs first): 4 nodes per warp, then warps
+        if (npu >= 2) val = val + __shfl_xor_sync(0xffffffffu, val, 8);
+        if (npu >= 4) val = val + __shfl_xor_sync(0xffffffffu, val, 16);
+        if ((tid & 31) == 0) sv[tid >> 5] = val;
+        __syncthreads();
+        if (tid == 0) {
+            const int cw = npu >= 4 ? npu / 4 : 1;
+            for (int st = 1; st < cw; st <<= 1)
+                for (int i = 0; i + st < cw; i += 2 * st) sv[i] = sv[i] + sv[i + st];
+            part[u] = sv[0];
+        }
+    }
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(&ctr[0], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    // perfect tree over the unit partials: up to 16 consecutive per thread in
+    // registers (the tree's lowest levels), then over the thread sums
+    const int m = (int)units;
+    const int per = m > 256 ? m / 256 : 1, cnt = m / per;
+    if (tid < cnt) {
+        double v[16];
+#pragma unroll
+        for (int k = 0; k < 16; k++) v[k] = k < per ? __ldcg(part + (int64_t)tid * per + k) : 0.0;
+#pragma unroll
+        for (int st = 1; st < 16; st <<= 1)
+#pragma unroll
+            for (int i = 0; i + st < 16; i += 2 * st)
+                if (i + st < per) v[i] = v[i] + v[i + st];
+        sv[tid] = v[0];
+    }
+    __syncthreads();
+    for (int st = 1; st < cnt; st <<= 1) {
+        for (int i = tid * 2 * st; i + st < cnt; i += blockDim.x * 2 * st) sv[i] = sv[i] + sv[i + st];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        dot_epilogue(sv[0], epi, nullptr, sc);
+        ctr[0] = 0u;
+        ctr[1] = 0u;
+    }
+}
+
+static int pw_cut_maxlen(int64_t n, int64_t *maxlen) {
+    std::vector<int64_t> sizes{n};
+    int cut = 0;
+    while (true) {
+        bool all_split = true;
+        for (int64_t s : sizes) all_split &= s > 128;
+        if (!all_split) break;
+        std::vector<int64_t> nxt;
+        for (int64_t s : sizes) {
+            const int64_t n2 = s / 2 - (s / 2) % 8;
+            nxt.push_back(n2);
+            nxt.push_back(s - n2);
+        }
+        std::sort(nxt.begin(), nxt.end());
+        nxt.erase(std::unique(nxt.begin(), nxt.end()), nxt.end());
+        sizes.swap(nxt);
+        cut++;
+    }
+    *maxlen = *std::max_element(sizes.begin(), sizes.end());
+    return cut;
+}
+
+// Plan of k_dot_staged for n rows; !ok when the shape is out of its range
+// (k_dot_fused then runs).
+static const StagedPlan &staged_plan(int64_t n) {
+    static thread_local StagedPlan P;
+    if (P.n == n) return P;
+    P = StagedPlan{};
+    P.n = n;
+    if (n <= 0) return P;
+    int64_t maxlen = 0;
+    P.cut = pw_cut_maxlen(n, &maxlen);
+    const int64_t nodes = (int64_t)1 << P.cut;
+    // 32 nodes per unit (every 8-lane group of the block sums one): 8 -> 49.7,
+    // 16 -> 49.25, 32 -> 48.98 ms/step at 256^3 (fewer barriers per row)
+    const int64_t npu = std::min<int64_t>(nodes, 32);
+    if (nodes / npu > kStagedMaxUnits) return P;
+    P.npu = (int)npu;
+    P.units = nodes / npu;
+    P.smem = maxlen * npu * (int64_t)sizeof(double);
+    if (P.smem > 48 * 1024) return P;
+    P.ok = true;
+    return P;
+}
+
+template <class F, int RB>
+static void launch_dot_staged(const F &f, int64_t n, double *tmp, int epi, DevScalars *sc,
+                              cudaStream_t st, int64_t *launches) {
+    const StagedPlan &P = staged_plan(n);
+    static thread_local int64_t occ_smem = -1;
+    static thread_local int per_sm = 1;
+    if (occ_smem != P.smem) {
+        occ_smem = P.smem;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dot_staged<F, RB>, 256,
+                                                          (size_t)P.smem) != cudaSuccess ||
+            per_sm < 1) {
+            cudaGetLastError();
+            per_sm = 1;
+        }
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(P.units, (int64_t)num_sms() * per_sm);
+    // tmp[1]: finish ticket + unit counter (zeroed at allocation, re-armed
+    // by the last block); unit partials from tmp + 2
+    launch_pdl(k_dot_staged<F, RB>, grid, 256, (size_t)P.smem, st, f, n, P.cut, P.npu, P.units,
+               tmp + 2, reinterpret_cast<unsigned *>(tmp + 1), epi, sc);
+    (*launches)++;
+}
+
 __global__ void k_fill(double *a, int64_t n, double v) {
     for (int64_t i = gtid(); i < n; i += gstride()) a[i] = v;
 }
@@ -1764,6 +1993,13 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     static const bool jfast_env = !getenv("FLIPB200_JACOBI_PLAIN");
     const bool jfast = cfg.solver == FLIP_SOLVER_JACOBI && !sl && S.meta && jfast_env;
     int64_t jit = 0;  // Jacobi iterations issued (buffer parity)
+    // PCG on one GPU: the z.r dot with the lane gather produces its summands
+    // row-coalesced (k_dot_staged: 35.6 -> ~26 us per iteration at 256^3);
+    // FLIPB200_STAGED_ZR=0 keeps k_dot_fused<LdLaneDot>
+    static const bool st_zr_env = !getenv("FLIPB200_STAGED_ZR") || atoi(getenv("FLIPB200_STAGED_ZR"));
+    const bool st_zr = !relax && !sl && nf > 0 && S.r0 == 0 && st_zr_env && staged_plan(n).ok;
+    static const bool st_sq_env = getenv("FLIPB200_STAGED_SQ") && atoi(getenv("FLIPB200_STAGED_SQ"));
+    const bool st_sq = st_zr && st_sq_env;
     // one iteration of SOLVERS[cfg.solver] (pressure.py:209-213 / 314-331)
     auto one_iter = [&]() {
         if (!relax) {  // pressure.py:314-331
@@ -1781,7 +2017,11 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 else
                     k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
                                                               nullptr, sc, 1);
-                solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
+                if (st_sq)
+                    launch_dot_staged<RowProd, 4>(RowProd{B.s, B.q}, n, B.dot_tmp, EPI_CURV, sc, st,
+                                                  launches);
+                else
+                    solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
                 (*launches)++;
             }
             launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
@@ -1796,7 +2036,12 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 (*launches)++;
             }
             apply_pc(S, cfg, B, LV, B.r, B.z, sc, st, launches, lane);
-            if (lane)
+            if (lane && st_zr) {
+                const RowLaneDot f{LV.lane->zL, LV.lane->posL, B.z, B.r,
+                                   lane_entries(LV.lane->args.geom)};
+                launch_dot_staged<RowLaneDot, 4>(f, n, B.dot_tmp, EPI_SIGMA_NEW, sc, st, launches);
+            }
+            else if (lane)
                 solver_dot(cfg, LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r, lane_entries(LV.lane->args.geom)}, nf, B.dot_tmp,
                            EPI_SIGMA_NEW, sc, st, launches);
             else
