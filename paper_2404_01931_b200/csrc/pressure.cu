@@ -1423,17 +1423,6 @@ struct LdSmem {
     __device__ __forceinline__ double operator()(int64_t i) const { return p[(int)(i - base)]; }
 };
 
-// a[i] * b[i] (LdProd), row-coalesced: the s.q dot (pressure.py:316)
-struct RowProd {
-    const double *__restrict__ a;
-    const double *__restrict__ b;
-    struct A { double x, y; };
-    struct B {};
-    __device__ __forceinline__ A pre(int64_t i) const { return {a[i], b[i]}; }
-    __device__ __forceinline__ B mid(int64_t, const A &) const { return {}; }
-    __device__ __forceinline__ double post(int64_t, const A &v, const B &) const { return v.x * v.y; }
-};
-
 // z from the lane-major layout of the MIC(0) sweep (LdLaneDot): z[r] written,
 // summand z[r] * r[r]: pressure.py:328-329.
 struct RowLaneDot {
@@ -1998,8 +1987,6 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
     // FLIPB200_STAGED_ZR=0 keeps k_dot_fused<LdLaneDot>
     static const bool st_zr_env = !getenv("FLIPB200_STAGED_ZR") || atoi(getenv("FLIPB200_STAGED_ZR"));
     const bool st_zr = !relax && !sl && nf > 0 && S.r0 == 0 && st_zr_env && staged_plan(n).ok;
-    static const bool st_sq_env = getenv("FLIPB200_STAGED_SQ") && atoi(getenv("FLIPB200_STAGED_SQ"));
-    const bool st_sq = st_zr && st_sq_env;
     // one iteration of SOLVERS[cfg.solver] (pressure.py:209-213 / 314-331)
     auto one_iter = [&]() {
         if (!relax) {  // pressure.py:314-331
@@ -2017,11 +2004,7 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 else
                     k_matvec<<<nblocks(n), kThreads, 0, st>>>(S, B.s, B.q, nullptr, nullptr,
                                                               nullptr, sc, 1);
-                if (st_sq)
-                    launch_dot_staged<RowProd, 4>(RowProd{B.s, B.q}, n, B.dot_tmp, EPI_CURV, sc, st,
-                                                  launches);
-                else
-                    solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
+                solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
                 (*launches)++;
             }
             launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
