@@ -2,6 +2,8 @@
 // key + histogram, binning, classification, G2P, reseeding and scene seeding.
 // Each kernel cites the reference function it re-implements; arithmetic is
 // written in the reference's association order (see common.cuh).
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace flip {
@@ -211,7 +213,9 @@ void stage_classify(Ctx &c) {
 
 // ------------------------------------------------------------------- G2P --
 // flipsim/transfer.py:60-82 with sample_velocity_many (_core.pyx:68-90).
-__global__ void k_g2p(ParticlePtrs P, int64_t n, Dims d, const double *__restrict__ un,
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_g2p(ParticlePtrs P, int64_t n, Dims d, const double *__restrict__ un,
                       const double *__restrict__ vn, const double *__restrict__ wn,
                       const double *__restrict__ uo, const double *__restrict__ vo,
                       const double *__restrict__ wo, double f) {
@@ -236,8 +240,12 @@ __global__ void k_g2p(ParticlePtrs P, int64_t n, Dims d, const double *__restric
 
 void stage_g2p(Ctx &c, const flip_step_params &prm) {
     if (c.n == 0) return;
-    k_g2p<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.d, c.u, c.v, c.w, c.uo, c.vo, c.wo,
-                                               prm.flip_fraction);
+    // 3 CTAs/SM (80 registers): 1.14 -> 0.93 ms/step at 256^3 (4: 0.98, 5 spills: 1.41,
+    // unbounded 126 registers: 1.14)
+    static const int minb = getenv("FLIPB200_G2P_MINB") ? atoi(getenv("FLIPB200_G2P_MINB")) : 3;
+    auto k = minb == 4 ? k_g2p<4> : minb == 5 ? k_g2p<5> : minb == 3 ? k_g2p<3> : k_g2p<1>;
+    k<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.d, c.u, c.v, c.w, c.uo, c.vo, c.wo,
+                                           prm.flip_fraction);
     c.launches++;
 }
 

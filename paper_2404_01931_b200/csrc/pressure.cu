@@ -1444,8 +1444,8 @@ struct RowLaneDot {
     }
 };
 
-template <class F, int RB>
-__global__ void __launch_bounds__(256)
+template <class F, int RB, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
 k_dot_staged(F f, int64_t n, int cut, int npu, int64_t units, double *__restrict__ part,
              unsigned *ctr, int epi, DevScalars *sc) {
     extern __shared__ double prod[];
@@ -1576,7 +1576,7 @@ static const StagedPlan &staged_plan(int64_t n) {
     return P;
 }
 
-template <class F, int RB>
+template <class F, int RB, int MINB = 1>
 static void launch_dot_staged(const F &f, int64_t n, double *tmp, int epi, DevScalars *sc,
                               cudaStream_t st, int64_t *launches) {
     const StagedPlan &P = staged_plan(n);
@@ -1584,7 +1584,7 @@ static void launch_dot_staged(const F &f, int64_t n, double *tmp, int epi, DevSc
     static thread_local int per_sm = 1;
     if (occ_smem != P.smem) {
         occ_smem = P.smem;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dot_staged<F, RB>, 256,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dot_staged<F, RB, MINB>, 256,
                                                           (size_t)P.smem) != cudaSuccess ||
             per_sm < 1) {
             cudaGetLastError();
@@ -1594,7 +1594,7 @@ static void launch_dot_staged(const F &f, int64_t n, double *tmp, int epi, DevSc
     const unsigned grid = (unsigned)std::min<int64_t>(P.units, (int64_t)num_sms() * per_sm);
     // tmp[1]: finish ticket + unit counter (zeroed at allocation, re-armed
     // by the last block); unit partials from tmp + 2
-    launch_pdl(k_dot_staged<F, RB>, grid, 256, (size_t)P.smem, st, f, n, P.cut, P.npu, P.units,
+    launch_pdl(k_dot_staged<F, RB, MINB>, grid, 256, (size_t)P.smem, st, f, n, P.cut, P.npu, P.units,
                tmp + 2, reinterpret_cast<unsigned *>(tmp + 1), epi, sc);
     (*launches)++;
 }
@@ -2022,7 +2022,9 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
             if (lane && st_zr) {
                 const RowLaneDot f{LV.lane->zL, LV.lane->posL, B.z, B.r,
                                    lane_entries(LV.lane->args.geom)};
-                launch_dot_staged<RowLaneDot, 4>(f, n, B.dot_tmp, EPI_SIGMA_NEW, sc, st, launches);
+                // 5 CTAs/SM (48 registers): PROJECT 37.86 -> 37.47 ms vs 66
+                // registers at 4; 6 (40, spills) 37.8
+                launch_dot_staged<RowLaneDot, 4, 5>(f, n, B.dot_tmp, EPI_SIGMA_NEW, sc, st, launches);
             }
             else if (lane)
                 solver_dot(cfg, LdLaneDot{LV.lane->zL, LV.lane->posL, B.z, B.r, lane_entries(LV.lane->args.geom)}, nf, B.dot_tmp,

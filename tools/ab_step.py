@@ -32,9 +32,12 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 torch.cuda.synchronize()
 e0.record(stream)
 proj = 0.0
+stages = {}
 for _ in range(K):
     rep = P.step(st, spec)
     proj += rep.timings.project
+    for k, v in vars(rep.timings).items():
+        stages[k] = stages.get(k, 0.0) + v
 e1.record(stream)
 e1.synchronize()
 ms = e0.elapsed_time(e1) / K
@@ -48,3 +51,5 @@ env = {k: v for k, v in os.environ.items() if k.startswith("FLIPB200_")}
 print(f"{env} res {res}: {ms:.2f} ms/step, project {proj / K:.2f} ms, "
       f"mic sweep {pms.value / max(pl.value, 1) * 1e3:.1f} us x {pl.value // K}/step, "
       f"its {rep.solver_iterations}, digest {h.hexdigest()[:16]}", flush=True)
+print("  stages (ms): " + ", ".join(f"{k} {v / K:.3f}" for k, v in stages.items() if k != "project"),
+      flush=True)
