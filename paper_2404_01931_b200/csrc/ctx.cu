@@ -163,6 +163,7 @@ int flip::realloc_particles(Ctx &c, int64_t cap, int64_t front) {
         const int64_t scan_n = std::max<int64_t>(radix_hist_ints(cap, c.ncells), c.ncells + 2);
         if (int rc = dalloc(&c.scan_tmp, scan_tmp_ints(scan_n) + 64)) return rc;
         c.keys_valid = 0;
+        c.pbox_valid = 0;
     }
     c.cap = cap;
     c.pfront = front;
@@ -431,6 +432,7 @@ extern "C" int flip_set_particles(flip_ctx *c, int64_t n, const double *px, cons
     for (int a = 0; a < 6; a++) TRY(h2d(c->P.a[a], src[a], sizeof(double) * n, c->st));
     c->n = n;
     c->keys_valid = 0;
+    c->pbox_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -481,6 +483,7 @@ extern "C" int flip_set_particle_count(flip_ctx *c, int64_t n) {
     }
     c->n = n;
     c->keys_valid = 0;
+    c->pbox_valid = 0;
     return 0;
 }
 
@@ -538,6 +541,7 @@ extern "C" int flip_set_particles_f32(flip_ctx *c, int64_t n, const float *in) {
     TRY(h2d(buf, in, sizeof(float) * 6 * n, c->st));
     c->n = n;
     c->keys_valid = 0;
+    c->pbox_valid = 0;
     launch_particles_f32(*c, buf, false);
     return flip_synchronize(c);
 }
@@ -559,6 +563,7 @@ extern "C" int flip_set_hash(flip_ctx *c, const int64_t *offset, const int64_t *
     cudaFree(o64);
     cudaFree(c64);
     c->keys_valid = 0;
+    c->pbox_valid = 0;
     return rc;
 }
 
@@ -610,6 +615,7 @@ extern "C" int flip_set_known(flip_ctx *c, const uint8_t *ku, const uint8_t *kv,
     TRY(h2d(c->kv, kv, c->nfv, c->st));
     TRY(h2d(c->kw, kw, c->nfw, c->st));
     c->known_valid = 1;
+    c->known_box = 0;
     return flip_synchronize(c);
 }
 
@@ -653,6 +659,7 @@ extern "C" int flip_seed_regions(flip_ctx *c, int32_t nregions, const flip_regio
     cudaSetDevice(c->device);
     TRY(seed_regions(*c, nregions, regions, rng_seed));
     c->keys_valid = 0;
+    c->pbox_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -768,6 +775,7 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
         std::swap(c->offset, c->offset2);
         c->n = c->sch->new_total;
         c->keys_valid = 0;
+        c->pbox_valid = 0;
     }
     int stop = status ? FLIP_STAGE_PROJECT : last;
     for (int s = first; s <= stop; s++) {

@@ -1,5 +1,7 @@
 // grid.cu — face-lattice stages: body force + wall enforcement, pressure
 // gradient subtract, layered velocity extrapolation, divergence.
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace flip {
@@ -213,6 +215,69 @@ __global__ void k_extrap_layer(double *__restrict__ A, double *__restrict__ B, L
     }
 }
 
+// k_extrap_layer over the faces that can change (one GPU, P2G known masks):
+// every known face lies within the particle cell box grown by one face
+// (a particle in cell c weights faces c, c+1 along the lattice's own axis and
+// c-1..c+1 across it), so after layer l-1 the known faces lie within that box
+// grown by l faces (V_l) and layer l fills faces within V_l grown by one
+// (B_l).  Layer l visits B_l only, reads its input mask inside V_l only
+// (outside it the face is unknown: for l >= 1 the scratch mask there is
+// stale), and writes its output mask over B_l, which is V_{l+1}.  Faces
+// outside B_l keep their values, as in the full-lattice kernel.  Same
+// neighbour order and arithmetic.
+__global__ void k_extrap_layer_box(double *__restrict__ A, double *__restrict__ B, Lat L,
+                                   const uint8_t *__restrict__ kin, uint8_t *__restrict__ kout,
+                                   const DevScalars *__restrict__ sc, int layer) {
+    if (sc->pbox_max[0] < 0) return;  // no particles: nothing is known
+    const int m[3] = {L.mx, L.my, L.mz};
+    int lo[3], hi[3], vlo[3], vhi[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        lo[a] = max(sc->pbox_min[a] - 2 - layer, 0);
+        hi[a] = min(sc->pbox_max[a] + 2 + layer, m[a] - 1);
+        vlo[a] = layer ? max(sc->pbox_min[a] - 1 - layer, 0) : 0;
+        vhi[a] = layer ? min(sc->pbox_max[a] + 1 + layer, m[a] - 1) : m[a] - 1;
+    }
+    const unsigned bx = hi[0] - lo[0] + 1, by = hi[1] - lo[1] + 1, bz = hi[2] - lo[2] + 1;
+    const unsigned V = bx * by * bz;
+    const int64_t sy = L.mx, sz = (int64_t)L.mx * L.my;
+    for (unsigned t = ugtid(); t < V; t += ugstride()) {
+        const unsigned q = t / bx, r = q / by;
+        const int i = lo[0] + (int)(t - q * bx), j = lo[1] + (int)(q - r * by), k = lo[2] + (int)r;
+        const int64_t f = i + j * sy + k * sz;
+        const bool in_v = i >= vlo[0] && i <= vhi[0] && j >= vlo[1] && j <= vhi[1] && k >= vlo[2] &&
+                          k <= vhi[2];
+        if (in_v && kin[f]) {
+            kout[f] = 1;
+            continue;
+        }
+        const int64_t nb[6] = {f + sz, f - sz, f + sy, f - sy, f + 1, f - 1};
+        // the neighbour is inside V (hence inside the lattice) and known
+        const bool ok[6] = {k + 1 <= vhi[2] && i >= vlo[0] && i <= vhi[0] && j >= vlo[1] && j <= vhi[1],
+                            k - 1 >= vlo[2] && i >= vlo[0] && i <= vhi[0] && j >= vlo[1] && j <= vhi[1],
+                            j + 1 <= vhi[1] && i >= vlo[0] && i <= vhi[0] && k >= vlo[2] && k <= vhi[2],
+                            j - 1 >= vlo[1] && i >= vlo[0] && i <= vhi[0] && k >= vlo[2] && k <= vhi[2],
+                            i + 1 <= vhi[0] && j >= vlo[1] && j <= vhi[1] && k >= vlo[2] && k <= vhi[2],
+                            i - 1 >= vlo[0] && j >= vlo[1] && j <= vhi[1] && k >= vlo[2] && k <= vhi[2]};
+        double a = 0.0, b = 0.0;
+        int cnt = 0;
+#pragma unroll
+        for (int qn = 0; qn < 6; qn++) {
+            const bool kn = ok[qn] && kin[nb[qn]];
+            cnt += kn;
+            a = a + (kn ? A[nb[qn]] : 0.0);
+            if (B) b = b + (kn ? B[nb[qn]] : 0.0);
+        }
+        if (cnt > 0) {
+            A[f] = a / (double)cnt;
+            if (B) B[f] = b / (double)cnt;
+            kout[f] = 1;
+        } else {
+            kout[f] = 0;
+        }
+    }
+}
+
 // pressure_field (pressure.py:49-53) is written by stage_project.
 // Slab mode: every kernel covers the own face planes, and the face planes
 // next to the slab are refreshed from the neighbours between the passes that
@@ -232,6 +297,9 @@ int stage_apply_gradient(Ctx &c, const flip_step_params &prm) {
         c.launches++;
     }
     const int layers = prm.extrapolation_layers;
+    // the layers visit the particle box only (FLIPB200_EXTRAP_BOX=0: every face)
+    static const bool box_env = !getenv("FLIPB200_EXTRAP_BOX") || atoi(getenv("FLIPB200_EXTRAP_BOX"));
+    const bool use_box = c.known_box && !c.slab.on && box_env;
     if (c.slab.on && layers > 0)
         if (int rc = slab_face_halo(c, SLAB_H_GRID)) return rc;
     for (int l = 0; l < layers; l++) {
@@ -239,8 +307,12 @@ int stage_apply_gradient(Ctx &c, const flip_step_params &prm) {
             Lat L = lat(c.d, comp);
             const uint8_t *kin = l == 0 ? k0[comp] : ((l - 1) & 1 ? s1[comp] : s0[comp]);
             uint8_t *kout = (l & 1) ? s1[comp] : s0[comp];
-            k_extrap_layer<<<nblocks(hi[comp] - lo[comp]), kThreads, 0, c.st>>>(
-                g[comp], o[comp], L, kin, kout, (unsigned)lo[comp], (unsigned)hi[comp]);
+            if (use_box)
+                k_extrap_layer_box<<<nblocks(hi[comp] - lo[comp]), kThreads, 0, c.st>>>(
+                    g[comp], o[comp], L, kin, kout, c.sc, l);
+            else
+                k_extrap_layer<<<nblocks(hi[comp] - lo[comp]), kThreads, 0, c.st>>>(
+                    g[comp], o[comp], L, kin, kout, (unsigned)lo[comp], (unsigned)hi[comp]);
             c.launches++;
         }
         if (c.slab.on && l + 1 < layers)

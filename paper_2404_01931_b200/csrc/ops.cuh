@@ -34,6 +34,7 @@ struct DevScalars {
     unsigned upd_ticket;                // k_pcg_update's last-block ticket (re-armed to 0)
     int x_it;                           // last iteration whose x += alpha s k_pcg_dir applied
     unsigned dir_ticket;                // k_pcg_dir's last-block ticket (re-armed to 0)
+    int pbox_min[3], pbox_max[3];       // cells holding particles (k_classify), inclusive
 };
 
 // CUDA-event bracketing of one kernel class (bench roofline evidence).
@@ -139,6 +140,8 @@ struct Ctx {
     Probe probe;
     int known_valid = 0;
     int keys_valid = 0;   // keys_sorted matches the current binned particles
+    int pbox_valid = 0;   // sc->pbox_* is the cell box of the current binned particles
+    int known_box = 0;    // the known masks vanish outside sc->pbox_* grown by one face
     Slab slab;
 };
 

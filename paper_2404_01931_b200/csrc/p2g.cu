@@ -10,6 +10,9 @@
 // grid_old.copy_velocities_from (grid.py:104-107), the known mask
 // (weights > 0, transfer.py:53), add_body_force (grid.py:193-202) and
 // enforce_solid_boundaries (grid.py:219-228).
+#include <climits>
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace flip {
@@ -62,7 +65,7 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
       const double *__restrict__ pz, const double *__restrict__ vel,
       const int *__restrict__ offset, const int *__restrict__ count, P2GOut out,
       const uint8_t *__restrict__ label, const DevScalars *__restrict__ sc, double g,
-      int fuse_force, unsigned f_lo, unsigned f_hi) {
+      int fuse_force, unsigned f_lo, unsigned f_hi, int use_box) {
     FaceLattice L = lattice(d, comp);
     // 32-bit index math: flip_create rejects grids with >= 2^31 faces;
     // [f_lo, f_hi): all faces, or the own planes of a slab
@@ -71,6 +74,17 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
     const int sxy = nx * ny;
     double gdt = 0.0;
     if (fuse_force && g != 0.0) gdt = g * sc->dt;
+    // faces whose candidate cells all lie outside the box of the cells
+    // holding particles (k_classify) gather nothing: num = dsum = 0, as the
+    // loop over their empty ranges would give
+    int blo[3] = {INT_MIN, INT_MIN, INT_MIN}, bhi[3] = {INT_MAX, INT_MAX, INT_MAX};
+    if (use_box) {
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            blo[a] = sc->pbox_min[a] - 1;
+            bhi[a] = sc->pbox_max[a] + 1;
+        }
+    }
     for (unsigned f = f_lo + blockIdx.x * blockDim.x + threadIdx.x; f < nf;
          f += gridDim.x * blockDim.x) {
         const unsigned fq = f / (unsigned)L.fnx;
@@ -84,6 +98,9 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
         int cylo = max(fj - 1, 0), cyhi = min(comp == 1 ? fj : fj + 1, ny - 1);
         int czlo = max(fk - 1, 0), czhi = min(comp == 2 ? fk : fk + 1, nz - 1);
         double num = 0.0, dsum = 0.0, cn = 0.0, cd = 0.0;
+        const bool empty = fi < blo[0] || fi > bhi[0] || fj < blo[1] || fj > bhi[1] || fk < blo[2] ||
+                           fk > bhi[2];
+        if (empty) czhi = czlo - 1;  // no candidate rows
         for (int cz = czlo; cz <= czhi; cz++) {
             for (int cy = cylo; cy <= cyhi; cy++) {
                 const int row = cy * nx + cz * sxy;
@@ -151,6 +168,8 @@ void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force) {
     uint8_t *known[3] = {c.ku, c.kv, c.kw};
     int64_t nf[3] = {c.nfu, c.nfv, c.nfw};
     (void)nf;
+    static const bool box_env = !getenv("FLIPB200_P2G_BOX") || atoi(getenv("FLIPB200_P2G_BOX"));
+    const bool use_box = c.pbox_valid && !c.slab.on && box_env;
     for (int comp = 0; comp < 3; comp++) {
         P2GOut o{grid[comp], old[comp], known[comp], nullptr};
         double g = prm ? prm->gravity[comp] : 0.0;
@@ -160,10 +179,11 @@ void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force) {
         // uniform branch and constant load less per hat (7.45 -> 6.50 ms/step)
         (c.d.pow2 ? k_p2g<true, 1> : k_p2g<true, 0>)<<<nblocks(f_hi - f_lo, kThreads, (int64_t)1 << 30), kThreads, 0, c.st>>>(
             c.d, comp, c.P.a[0], c.P.a[1], c.P.a[2], c.P.a[3 + comp], c.offset, nullptr, o,
-            c.label, c.sc, g, fuse_force, (unsigned)f_lo, (unsigned)f_hi);
+            c.label, c.sc, g, fuse_force, (unsigned)f_lo, (unsigned)f_hi, use_box ? 1 : 0);
         c.launches++;
     }
     c.known_valid = 1;
+    c.known_box = c.pbox_valid && !c.slab.on;  // known faces lie within the particle box + 1
 }
 
 void stage_p2g(Ctx &c, const flip_step_params &prm) { stage_p2g_impl(c, &prm, 0); }
@@ -175,7 +195,7 @@ void launch_p2g_component(const Dims &d, int comp, const double *vel, const doub
     int64_t nf = (int64_t)L.fnx * L.fny * L.fnz;
     P2GOut o{out, nullptr, nullptr, den};
     k_p2g<false><<<nblocks(nf, kThreads, (int64_t)1 << 30), kThreads, 0, st>>>(
-        d, comp, px, py, pz, vel, offset, count, o, nullptr, nullptr, 0.0, 0, 0u, (unsigned)nf);
+        d, comp, px, py, pz, vel, offset, count, o, nullptr, nullptr, 0.0, 0, 0u, (unsigned)nf, 0);
 }
 
 }  // namespace flip

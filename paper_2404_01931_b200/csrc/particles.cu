@@ -2,6 +2,7 @@
 // key + histogram, binning, classification, G2P, reseeding and scene seeding.
 // Each kernel cites the reference function it re-implements; arithmetic is
 // written in the reference's association order (see common.cuh).
+#include <climits>
 #include <cstdlib>
 
 #include "ops.cuh"
@@ -172,6 +173,7 @@ __global__ void k_keys_count(ParticlePtrs P, int64_t n, Dims d, int *__restrict_
 }
 
 void stage_bin_from_keys(Ctx &c) {
+    c.pbox_valid = 0;  // the counts change: k_classify recomputes the box
     // offset = exclusive_scan(count) (binning.py:91); offset[ncells] = N
     exclusive_scan(ArrayIn{c.count}, c.ncells, c.offset, c.offset + c.ncells, c.scan_tmp, c.st);
     c.launches += 3;
@@ -197,18 +199,72 @@ void stage_bin(Ctx &c) {
 
 // -------------------------------------------------------------- classify --
 // flipsim/grid.py:185-190
-__global__ void k_classify(uint8_t *__restrict__ label, const int *__restrict__ count, int64_t nc) {
+// Also the box of the cells that hold particles (sc->pbox_*, BOX), which
+// bounds the P2G known masks for the extrapolation (grid.cu).
+template <bool BOX>
+__global__ void k_classify(uint8_t *__restrict__ label, const int *__restrict__ count, int64_t nc,
+                           Dims d, DevScalars *sc) {
+    int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {-1, -1, -1};
     for (int64_t c = gtid(); c < nc; c += gstride()) {
         uint8_t l = label[c];
-        if (l != SOLID) label[c] = count[c] > 0 ? FLUID : AIR;
+        const int cnt = count[c];
+        if (l != SOLID) label[c] = cnt > 0 ? FLUID : AIR;
+        if (BOX && cnt > 0) {
+            int ijk[3];
+            cell_ijk(d, c, ijk[0], ijk[1], ijk[2]);
+#pragma unroll
+            for (int a = 0; a < 3; a++) {
+                mn[a] = min(mn[a], ijk[a]);
+                mx[a] = max(mx[a], ijk[a]);
+            }
+        }
+    }
+    if (!BOX) return;
+    __shared__ int smn[3], smx[3];
+    if (threadIdx.x < 3) {
+        smn[threadIdx.x] = INT_MAX;
+        smx[threadIdx.x] = -1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        for (int o = 16; o; o >>= 1) {
+            mn[a] = min(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = max(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+        if ((threadIdx.x & 31) == 0 && mx[a] >= 0) {
+            atomicMin(&smn[a], mn[a]);
+            atomicMax(&smx[a], mx[a]);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3 && smx[threadIdx.x] >= 0) {
+        atomicMin(&sc->pbox_min[threadIdx.x], smn[threadIdx.x]);
+        atomicMax(&sc->pbox_max[threadIdx.x], smx[threadIdx.x]);
+    }
+}
+
+__global__ void k_pbox_reset(DevScalars *sc) {
+    for (int a = 0; a < 3; a++) {
+        sc->pbox_min[a] = INT_MAX;
+        sc->pbox_max[a] = -1;
     }
 }
 
 void stage_classify(Ctx &c) {
     // slab mode: the own cells only (the other planes arrive by slab_labels)
     const int64_t c0 = c.slab.on ? c.slab_c0 : 0, c1 = c.slab.on ? c.slab_c1 : c.ncells;
-    k_classify<<<nblocks(c1 - c0), kThreads, 0, c.st>>>(c.label + c0, c.count + c0, c1 - c0);
-    c.launches++;
+    if (c.slab.on) {
+        k_classify<false><<<nblocks(c1 - c0), kThreads, 0, c.st>>>(c.label + c0, c.count + c0,
+                                                                   c1 - c0, c.d, c.sc);
+        c.launches++;
+        c.pbox_valid = 0;
+        return;
+    }
+    k_pbox_reset<<<1, 1, 0, c.st>>>(c.sc);
+    k_classify<true><<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.label, c.count, c.ncells, c.d, c.sc);
+    c.launches += 2;
+    c.pbox_valid = 1;
 }
 
 // ------------------------------------------------------------------- G2P --
@@ -366,6 +422,7 @@ __global__ void k_reseed_emit(ParticlePtrs Q, Dims d, const int *__restrict__ co
 }
 
 int stage_reseed(Ctx &c, const flip_step_params &prm) {
+    c.pbox_valid = 0;
     int *new_count = c.count2, *new_offset = c.offset2, *nadd = c.nadd;
     cudaMemsetAsync(&c.sc->reseed_changed, 0, sizeof(int), c.st);
     const int64_t c1 = c.slab_c1 < 0 ? c.ncells : c.slab_c1;
