@@ -205,8 +205,10 @@ __device__ __forceinline__ double uniform01(uint64_t seed, uint64_t stream, uint
 __device__ __forceinline__ void jitter_pos(const Dims &d, int64_t c, int64_t s, int density,
                                            uint64_t seed, double &px, double &py, double &pz) {
     double sub_len = d.dtau / (double)density;
-    int64_t ci = c % d.nx, cj = (c / d.nx) % d.ny, ck = c / ((int64_t)d.nx * d.ny);
-    int64_t si = s % density, sj = (s / density) % density, sk = s / ((int64_t)density * density);
+    int ci, cj, ck;  // cell counts are below 2^31 (flip_create): 32-bit division
+    cell_ijk(d, c, ci, cj, ck);
+    const int si32 = (int)s;
+    int si = si32 % density, sj = (si32 / density) % density, sk = si32 / (density * density);
     double jx = uniform01(seed, (uint64_t)c, (uint64_t)(s * 4 + 0));
     double jy = uniform01(seed, (uint64_t)c, (uint64_t)(s * 4 + 1));
     double jz = uniform01(seed, (uint64_t)c, (uint64_t)(s * 4 + 2));
