@@ -219,6 +219,12 @@ extern "C" void flip_destroy(flip_ctx *c) {
     for (auto &e : c->probe.ev)
         if (e) cudaEventDestroy(e);
     if (c->st) cudaStreamDestroy(c->st);
+    if (c->st2) {
+        cudaStreamSynchronize(c->st2);
+        cudaStreamDestroy(c->st2);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_side) cudaEventDestroy(c->ev_side);
     delete c;
 }
 
@@ -241,9 +247,12 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     FLIP_CUDA_OK(cudaSetDevice(device));
     flip_ctx *c = new flip_ctx();
     c->device = device;
-    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming) != cudaSuccess) {
         set_error("cudaStreamCreate failed");
-        delete c;
+        flip_destroy(c);
         return FLIP_E_CUDA;
     }
     c->d = make_dims(nx, ny, nz, dtau, origin);
@@ -687,6 +696,7 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
     int64_t launches0 = c->launches;
     bool keys_from_advect = false, force_fused = false, reseed_ran = false;
     int status = 0;
+    c->proj_pre = 0;
     // NVTX: one range per stage (StageTimings keys, sim.py:24-46), visible
     // to nsys / ncu --nvtx; a no-op without an attached tool
     static const char *kStageNames[FLIP_NSTAGES] = {
@@ -726,6 +736,9 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
                 force_fused = last >= FLIP_STAGE_FORCE;
                 if (c->slab.on)
                     if (int rc = slab_ghosts(*c)) return rc;
+                // the pressure system's structure depends on the labels only:
+                // built on the side stream while P2G runs
+                if (last >= FLIP_STAGE_PROJECT) project_prefetch(*c);
                 stage_p2g_impl(*c, prm, force_fused ? 1 : 0);
                 if (c->slab.on) {
                     slab_ghosts_clear(*c);

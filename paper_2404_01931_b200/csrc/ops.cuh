@@ -84,6 +84,11 @@ struct Slab {
 struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;
+    // side stream: the pressure system's structure (union-find, row numbering,
+    // neighbours) runs there while P2G runs on st (project_prefetch)
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_side = nullptr;
+    int proj_pre = 0;  // project_prefetch issued the structure phase for this step
     Dims d{};
     int64_t ncells = 0, nfu = 0, nfv = 0, nfw = 0;
     int64_t cap = 0;        // particle capacity (entries from P.a[a][0])
@@ -164,6 +169,7 @@ void stage_p2g(Ctx &c, const flip_step_params &prm);   // + grid_old copy, known
 void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force);
 void stage_force(Ctx &c, const flip_step_params &prm); // body force + enforce
 int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep);  // syncs
+void project_prefetch(Ctx &c);  // structure phase of stage_project on c.st2 (one GPU)
 int stage_apply_gradient(Ctx &c, const flip_step_params &prm);
 void stage_g2p(Ctx &c, const flip_step_params &prm);
 int stage_reseed(Ctx &c, const flip_step_params &prm);

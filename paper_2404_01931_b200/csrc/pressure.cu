@@ -184,6 +184,7 @@ __global__ void k_rows_compact(IsRowIn in, int64_t nc, const int *__restrict__ r
 
 // Per-row diag, neighbour rows (order -x,+x,-y,+y,-z,+z, pressure.py:25) and
 // rhs = -div with solid faces zeroed (pressure.py:144-151).
+template <bool STRUCT, bool RHS>
 __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
                                 const uint8_t *__restrict__ isrow, const int *__restrict__ rowscan,
                                 const int *__restrict__ cell_of_row, const DevScalars *sc,
@@ -212,15 +213,18 @@ __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
             uint8_t l = lab_at(label, d, ii, jj, kk);
             nl[q] = l;
             ns += l != SOLID;
-            int nb = -1;
-            if (l == FLUID) {
-                int64_t cc = ii + (int64_t)jj * d.nx + kk * sxy;
-                if (isrow[cc]) nb = rowscan[cc];
+            if (STRUCT) {
+                int nb = -1;
+                if (l == FLUID) {
+                    int64_t cc = ii + (int64_t)jj * d.nx + kk * sxy;
+                    if (isrow[cc]) nb = rowscan[cc];
+                }
+                nbr[q * ldn + r] = nb;
             }
-            nbr[q * ldn + r] = nb;
         }
-        diag[r] = (double)ns;
-        if (r >= rhs_lo && r < rhs_hi) {
+        if (STRUCT) diag[r] = (double)ns;
+        if (!RHS) {
+        } else if (r >= rhs_lo && r < rhs_hi) {
             int64_t fu0 = i + (int64_t)j * (d.nx + 1) + (int64_t)k * (d.nx + 1) * d.ny;
             int64_t fv0 = i + (int64_t)j * d.nx + (int64_t)k * d.nx * (d.ny + 1);
             int64_t fw0 = c;
@@ -241,8 +245,11 @@ __global__ void k_assemble_rows(Dims d, const uint8_t *__restrict__ label,
         lo[1] = min(lo[1], j); hi[1] = max(hi[1], j);
         lo[2] = min(lo[2], k); hi[2] = max(hi[2], k);
     }
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(rhsmax, m);
+    if (RHS) {
+        for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_nonneg(rhsmax, m);
+    }
+    if (!STRUCT) return;
     // bounding box of the rows (wavefront geometry)
     for (int a = 0; a < 3; a++) {
         for (int o = 16; o; o >>= 1) {
@@ -2202,11 +2209,11 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
 // ============================================================ step: project
 // assemble (pressure.py:76-166) + SOLVERS[cfg.solver] (sim.py:266-270) +
 // grid.p = pressure_field(x) (sim.py:274).  Syncs to learn the row count.
-int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
-    cudaStream_t st = c.st;
+// Sealed-region pinning (union-find over the labels), row numbering and
+// compaction, reset of the row box (pressure.py:76-166 before the rhs).
+static void project_rows(Ctx &c, cudaStream_t st) {
     int64_t nc = c.ncells;
     cudaMemsetAsync(&c.sc->npinned, 0, sizeof(int), st);
-    cudaMemsetAsync(&c.sc->rhsmax_bits, 0, sizeof(unsigned long long), st);
     static const bool uf_plain = getenv("FLIPB200_UF_PLAIN") != nullptr;
     if (uf_plain) {
         k_uf_init<<<nblocks(nc), kThreads, 0, st>>>(c.label, nc, c.parent, c.has_air);
@@ -2222,12 +2229,49 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
     k_rows_compact<<<nblocks(nc), kThreads, 0, st>>>(in, nc, c.rowscan, c.isrow, c.cell_of_row, c.sc);
     k_bbox_reset<<<1, 1, 0, st>>>(c.sc);
     c.launches += 6;
+}
+
+// The rows, their neighbours and diagonal depend on the labels only, so
+// they are built on the side stream while P2G runs on the main stream (one
+// GPU; FLIPB200_PROJECT_OVERLAP=0 keeps them inside stage_project).  The
+// rhs needs the P2G velocities and is assembled by stage_project.
+void project_prefetch(Ctx &c) {
+    static const bool env = !getenv("FLIPB200_PROJECT_OVERLAP") ||
+                            atoi(getenv("FLIPB200_PROJECT_OVERLAP"));
+    if (c.slab.on || !env) return;
+    cudaEventRecord(c.ev_fork, c.st);  // labels final (classify)
+    cudaStreamWaitEvent(c.st2, c.ev_fork, 0);
+    project_rows(c, c.st2);
+    k_assemble_rows<true, false><<<nblocks(c.ncells), kThreads, 0, c.st2>>>(
+        c.d, c.label, c.isrow, c.rowscan, c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr, c.ncells,
+        c.diagd, c.rhs, &c.sc->rhsmax_bits, c.sc, (int64_t)0, (int64_t)-1, (int64_t)0, (int64_t)-1);
+    c.launches++;
+    cudaMemcpyAsync(c.sch, c.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c.st2);
+    cudaEventRecord(c.ev_side, c.st2);
+    c.proj_pre = 1;
+}
+
+int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
+    cudaStream_t st = c.st;
+    int64_t nc = c.ncells;
+    cudaMemsetAsync(&c.sc->rhsmax_bits, 0, sizeof(unsigned long long), st);
+    const bool pre = c.proj_pre != 0;
+    c.proj_pre = 0;
+    if (!pre) project_rows(c, st);
     bool need_sweeps = prm.solver == FLIP_SOLVER_GS ||
                        (prm.solver == FLIP_SOLVER_PCG && prm.precond == FLIP_PRECOND_MIC0);
     Slab &SL = c.slab;
     SlabDot SD{&c};
-    if (!SL.on) {
-        k_assemble_rows<<<nblocks(nc), kThreads, 0, st>>>(c.d, c.label, c.isrow, c.rowscan,
+    if (pre) {
+        // structure from project_prefetch; the rhs from the P2G velocities
+        FLIP_CUDA_OK(cudaEventSynchronize(c.ev_side));
+        cudaStreamWaitEvent(st, c.ev_side, 0);
+        k_assemble_rows<false, true><<<nblocks(nc), kThreads, 0, st>>>(
+            c.d, c.label, c.isrow, c.rowscan, c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr, nc, c.diagd,
+            c.rhs, &c.sc->rhsmax_bits, c.sc, (int64_t)0, (int64_t)-1, (int64_t)0, (int64_t)-1);
+        c.launches++;
+    } else if (!SL.on) {
+        k_assemble_rows<true, true><<<nblocks(nc), kThreads, 0, st>>>(c.d, c.label, c.isrow, c.rowscan,
                                                           c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr,
                                                           nc, c.diagd, c.rhs, &c.sc->rhsmax_bits,
                                                           c.sc, (int64_t)0, (int64_t)-1,
@@ -2242,14 +2286,16 @@ int stage_project(Ctx &c, const flip_step_params &prm, flip_step_report *rep) {
         // structure (diag, neighbours, bounding box) of every row when a
         // replicated sweep needs it, else of the window; rhs of the own rows
         const int64_t a_lo = full ? 0 : SL.Rlo, a_hi = full ? SL.rstart[SL.world] : SL.Rhi;
-        k_assemble_rows<<<nblocks(std::max<int64_t>(a_hi - a_lo, 1)), kThreads, 0, st>>>(
+        k_assemble_rows<true, true><<<nblocks(std::max<int64_t>(a_hi - a_lo, 1)), kThreads, 0, st>>>(
             c.d, c.label, c.isrow, c.rowscan, c.cell_of_row, c.sc, c.u, c.v, c.w, c.nbr, nc,
             c.diagd, c.rhs, &c.sc->rhsmax_bits, c.sc, a_lo, a_hi, SL.R0, SL.R1);
         c.launches++;
         if (int rc = slab_allreduce(c, (int64_t *)&c.sc->rhsmax_bits, 1, FLIP_OP_MAX)) return rc;
     }
-    cudaMemcpyAsync(c.sch, c.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
-    FLIP_CUDA_OK(cudaStreamSynchronize(st));
+    if (!pre) {
+        cudaMemcpyAsync(c.sch, c.sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st);
+        FLIP_CUDA_OK(cudaStreamSynchronize(st));
+    }
     int64_t n = c.sch->nrows;
     double dt = c.sch->dt;
     rep->nrows = n;
