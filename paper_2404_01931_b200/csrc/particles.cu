@@ -89,7 +89,9 @@ __global__ void k_box_final(Dims d, DevScalars *sc) {
 
 // flipsim/particles.py:227-248 (forward Euler + per-axis clamp), fused with
 // cell_index_many (binning.py:37-42) and the per-cell count (binning.py:90).
-__global__ void k_advect_key(ParticlePtrs P, int64_t n, const DevScalars *__restrict__ sc,
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_advect_key(ParticlePtrs P, int64_t n, const DevScalars *__restrict__ sc,
                              double skin, Dims d, int *__restrict__ keys, int *__restrict__ count) {
     double dt = sc->dt;
     double lo[3] = {sc->lo[0], sc->lo[1], sc->lo[2]}, hi[3] = {sc->hi[0], sc->hi[1], sc->hi[2]};
@@ -155,8 +157,9 @@ void stage_advect(Ctx &c, const flip_step_params &prm) {
                                                               c.v, c.w, c.keys0, c.count);
         c.launches++;
     } else if (c.n > 0) {
-        k_advect_key<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.sc, prm.skin_h, c.d, c.keys0,
-                                                          c.count);
+        static const int minb = getenv("FLIPB200_ADVECT_MINB") ? atoi(getenv("FLIPB200_ADVECT_MINB")) : 3;
+        auto k = minb == 4 ? k_advect_key<4> : minb == 6 ? k_advect_key<6> : minb == 8 ? k_advect_key<8> : k_advect_key<3>;
+        k<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.sc, prm.skin_h, c.d, c.keys0, c.count);
         c.launches++;
     }
 }

@@ -4,6 +4,8 @@
 // unique permutation the reference's sequential cursor scatter produces, so
 // the particle order is byte-identical.  Plus the scan partials kernel and
 // the six-array gather of ParticleSet.reorder (particles.py:54-64).
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace flip {
@@ -53,7 +55,9 @@ __global__ void k_radix_hist(const int *__restrict__ keys, int64_t n, int shift,
 // digit are ranked by lane with __match_any_sync, so each warp's ranks are
 // stable; per-(warp, digit) counts are then prefix-summed across warps in
 // warp order, which keeps the whole tile stable.
-__global__ void k_radix_scatter(const int *__restrict__ keys_in, const int *__restrict__ vals_in,
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+k_radix_scatter(const int *__restrict__ keys_in, const int *__restrict__ vals_in,
                                 int64_t n, int shift, int nbits, int ntiles,
                                 const int *__restrict__ hist_scanned, int *__restrict__ keys_out,
                                 int *__restrict__ vals_out) {
@@ -151,8 +155,9 @@ int radix_sort_cells(int *k0, int *k1, int *v0, int *v1, int64_t n, int64_t ncel
         int shift = p * nbits;
         k_radix_hist<<<ntiles, kThreads, sh_hist, st>>>(kin, n, shift, nbits, ntiles, hist);
         exclusive_scan(ArrayIn{hist}, (int64_t)nb * ntiles, hist, scan_total, scan_tmp, st);
-        k_radix_scatter<<<ntiles, kThreads, sh_scat, st>>>(kin, vin, n, shift, nbits, ntiles, hist,
-                                                         kout, vout);
+        static const int minb = getenv("FLIPB200_SCATTER_MINB") ? atoi(getenv("FLIPB200_SCATTER_MINB")) : 3;
+        auto ks = minb == 4 ? k_radix_scatter<4> : minb == 2 ? k_radix_scatter<2> : k_radix_scatter<3>;
+        ks<<<ntiles, kThreads, sh_scat, st>>>(kin, vin, n, shift, nbits, ntiles, hist, kout, vout);
         *launches += 5;
         int *tk = kin;
         kin = kout;
