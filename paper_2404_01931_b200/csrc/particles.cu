@@ -157,7 +157,8 @@ void stage_advect(Ctx &c, const flip_step_params &prm) {
                                                               c.v, c.w, c.keys0, c.count);
         c.launches++;
     } else if (c.n > 0) {
-        static const int minb = getenv("FLIPB200_ADVECT_MINB") ? atoi(getenv("FLIPB200_ADVECT_MINB")) : 3;
+        // 8 CTAs/SM (32 registers): ADVECT 0.588 -> 0.351 ms (4: 0.475, 6: 0.413)
+        static const int minb = getenv("FLIPB200_ADVECT_MINB") ? atoi(getenv("FLIPB200_ADVECT_MINB")) : 8;
         auto k = minb == 4 ? k_advect_key<4> : minb == 6 ? k_advect_key<6> : minb == 8 ? k_advect_key<8> : k_advect_key<3>;
         k<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.n, c.sc, prm.skin_h, c.d, c.keys0, c.count);
         c.launches++;

@@ -436,8 +436,8 @@ __global__ void k_dot_tree(const double *__restrict__ in, int64_t cnt, double *_
 // block (<= 1024): every block publishes its partial, the last block to
 // finish (threadfence + ticket) runs k_dot_tree's perfect-tree reduction and
 // the epilogue, then re-arms the ticket.  Same summation order.
-template <class LD>
-__global__ void __launch_bounds__(256, kDotBlocksPerSM)
+template <class LD, int MINB = kDotBlocksPerSM>
+__global__ void __launch_bounds__(256, MINB)
 k_dot_fused(LD ld, int64_t n, int cut, double *__restrict__ part, unsigned *ticket, int epi,
             DevScalars *sc, double *final_out, int skip_when_done) {
     pdl_wait();
@@ -547,9 +547,11 @@ static void launch_dot_f(const LD &ld, int64_t n, double *tmp, double *out_dev, 
     if (nb1 <= 1024) {
         // ticket zeroed at allocation and re-armed to 0 by the last block
         unsigned *ticket = reinterpret_cast<unsigned *>(tmp);
-        const unsigned grid = (unsigned)std::min<int64_t>(nb1, (int64_t)num_sms() * kDotBlocksPerSM);
-        launch_pdl(k_dot_fused<LD>, grid, 256, 0, st, ld, n, cut, p0, ticket, epi, sc, out_dev,
-                   skip ? 1 : 0);
+        static const int dminb = getenv("FLIPB200_DOT_MINB") ? atoi(getenv("FLIPB200_DOT_MINB")) : kDotBlocksPerSM;
+        const int per_sm = dminb == 6 ? 6 : dminb == 8 ? 8 : kDotBlocksPerSM;
+        const unsigned grid = (unsigned)std::min<int64_t>(nb1, (int64_t)num_sms() * per_sm);
+        auto kd = per_sm == 6 ? k_dot_fused<LD, 6> : per_sm == 8 ? k_dot_fused<LD, 8> : k_dot_fused<LD>;
+        launch_pdl(kd, grid, 256, 0, st, ld, n, cut, p0, ticket, epi, sc, out_dev, skip ? 1 : 0);
         (*launches)++;
         return;
     }
@@ -1225,7 +1227,8 @@ __device__ __forceinline__ void iter_check_body(DevScalars *sc, int64_t max_iter
 // convergence test (k_iter_check's body), so the PCG loop needs no separate
 // check launch.  x += alpha s (pressure.py:322) is applied by k_pcg_dir,
 // which reads s anyway (one pass over s per iteration instead of two).
-__global__ void __launch_bounds__(256)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB)
 k_pcg_update(int64_t n, double *__restrict__ r, const double *__restrict__ q, DevScalars *sc,
              double *__restrict__ rL, const int *__restrict__ posL, int64_t max_iters,
              double *history, int check, HaloReset H) {
@@ -2014,7 +2017,9 @@ static int run_solve(const SysView &S, const SolveCfg &cfg, const SolveBufs &B,
                 solver_dot(cfg, LdProd{B.s, B.q}, nf, B.dot_tmp, EPI_CURV, sc, st, launches);
                 (*launches)++;
             }
-            launch_pdl(k_pcg_update, wave_blocks(k_pcg_update, n), kThreads, 0, st, n,
+            static const int upd_minb = getenv("FLIPB200_UPDATE_MINB") ? atoi(getenv("FLIPB200_UPDATE_MINB")) : 1;
+            auto kupd = upd_minb == 6 ? k_pcg_update<6> : upd_minb == 8 ? k_pcg_update<8> : k_pcg_update<1>;
+            launch_pdl(kupd, wave_blocks(kupd, n), kThreads, 0, st, n,
                        B.r + o, (const double *)(B.q + o), sc,
                        (lane && !sl) ? LV.lane->rL : nullptr,
                        (lane && !sl) ? (const int *)LV.lane->posL : nullptr,
