@@ -697,6 +697,18 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
     bool keys_from_advect = false, force_fused = false, reseed_ran = false;
     int status = 0;
     c->proj_pre = 0;
+    // a prefetched pressure structure (project_prefetch, side stream) that
+    // stage_project did not consume (an error between P2G and PROJECT): the
+    // main stream waits for it, so no later call races with the side stream
+    struct SideJoin {
+        flip_ctx *c;
+        ~SideJoin() {
+            if (c->proj_pre) {
+                cudaStreamWaitEvent(c->st, c->ev_side, 0);
+                c->proj_pre = 0;
+            }
+        }
+    } side_join{c};
     // NVTX: one range per stage (StageTimings keys, sim.py:24-46), visible
     // to nsys / ncu --nvtx; a no-op without an attached tool
     static const char *kStageNames[FLIP_NSTAGES] = {
