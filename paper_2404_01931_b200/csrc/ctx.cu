@@ -164,6 +164,7 @@ int flip::realloc_particles(Ctx &c, int64_t cap, int64_t front) {
         if (int rc = dalloc(&c.scan_tmp, scan_tmp_ints(scan_n) + 64)) return rc;
         c.keys_valid = 0;
         c.pbox_valid = 0;
+        c.prec_valid = 0;
     }
     c.cap = cap;
     c.pfront = front;
@@ -212,6 +213,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->sch) cudaFreeHost(c->sch);
+    if (c->prec) cudaFree(c->prec);
     if (c->probe.ts) cudaFree(c->probe.ts);
     if (c->probe.ts_host) cudaFreeHost(c->probe.ts_host);
     for (auto &e : c->ev)
@@ -442,6 +444,7 @@ extern "C" int flip_set_particles(flip_ctx *c, int64_t n, const double *px, cons
     c->n = n;
     c->keys_valid = 0;
     c->pbox_valid = 0;
+    c->prec_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -493,6 +496,7 @@ extern "C" int flip_set_particle_count(flip_ctx *c, int64_t n) {
     c->n = n;
     c->keys_valid = 0;
     c->pbox_valid = 0;
+    c->prec_valid = 0;
     return 0;
 }
 
@@ -551,6 +555,7 @@ extern "C" int flip_set_particles_f32(flip_ctx *c, int64_t n, const float *in) {
     c->n = n;
     c->keys_valid = 0;
     c->pbox_valid = 0;
+    c->prec_valid = 0;
     launch_particles_f32(*c, buf, false);
     return flip_synchronize(c);
 }
@@ -573,6 +578,7 @@ extern "C" int flip_set_hash(flip_ctx *c, const int64_t *offset, const int64_t *
     cudaFree(c64);
     c->keys_valid = 0;
     c->pbox_valid = 0;
+    c->prec_valid = 0;
     return rc;
 }
 
@@ -669,6 +675,7 @@ extern "C" int flip_seed_regions(flip_ctx *c, int32_t nregions, const flip_regio
     TRY(seed_regions(*c, nregions, regions, rng_seed));
     c->keys_valid = 0;
     c->pbox_valid = 0;
+    c->prec_valid = 0;
     return flip_synchronize(c);
 }
 
@@ -801,6 +808,7 @@ extern "C" int flip_run_stages(flip_ctx *c, const flip_step_params *prm, int32_t
         c->n = c->sch->new_total;
         c->keys_valid = 0;
         c->pbox_valid = 0;
+        c->prec_valid = 0;
     }
     int stop = status ? FLIP_STAGE_PROJECT : last;
     for (int s = first; s <= stop; s++) {

@@ -92,6 +92,12 @@ struct Ctx {
     Dims d{};
     int64_t ncells = 0, nfu = 0, nfv = 0, nfw = 0;
     int64_t cap = 0;        // particle capacity (entries from P.a[a][0])
+    // P2G particle records: rec[comp][i] = {x, y, z, v_comp} (32 B, one 256-bit
+    // load per candidate), written by the bin gather; prec_valid while they
+    // match the binned particles
+    double *prec = nullptr;
+    int64_t prec_cap = 0;
+    int prec_valid = 0;
     int64_t pfront = 0;     // extra entries before P.a[a][0] (slab ghost plane below)
     int64_t n = 0;          // particle count (host mirror)
     int64_t slab_c0 = 0, slab_c1 = -1;  // reseed cell range (flip_set_slab); -1: all
@@ -154,6 +160,8 @@ struct Ctx {
 __global__ void k_iota(int *a, int64_t n);
 __global__ void k_gather6(ParticlePtrs src, ParticlePtrs dst, const int *__restrict__ perm,
                           int64_t n);
+__global__ void k_gather6_rec(ParticlePtrs src, ParticlePtrs dst, const int *__restrict__ perm,
+                              int64_t n, double *__restrict__ rec, int64_t ld);
 int64_t radix_hist_ints(int64_t cap, int64_t ncells);
 int radix_sort_cells(int *k0, int *k1, int *v0, int *v1, int64_t n, int64_t ncells, int *hist,
                      int *scan_tmp, int *scan_total, cudaStream_t st, int **keys_sorted,

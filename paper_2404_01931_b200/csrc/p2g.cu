@@ -59,7 +59,16 @@ struct P2GOut {
 // the Cython signature, used by the plugin API.
 // MINB 5 (48 registers, no spill since the power-of-two test left the
 // loop): P2G 6.44 -> 6.12 ms/step; 6 (40 registers): 6.29, 8: 7.38
-template <bool CONTIG, int P2 = 0, int MINB = 5>
+__device__ __forceinline__ void ld_rec(const double *p, double &x, double &y, double &z, double &v) {
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(x), "=d"(y), "=d"(z), "=d"(v)
+                 : "l"(p));
+}
+
+// REC: candidates read from the bin gather's records {x, y, z, v_comp} (one
+// 256-bit load instead of four 8-byte loads: the walk is bound by L1
+// wavefronts, ~16 per scattered 8-byte warp load); rec = px (+ 4 t).
+template <bool CONTIG, int P2 = 0, int MINB = 5, bool REC = false>
 __global__ void __launch_bounds__(kThreads, MINB)
 k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict__ py,
       const double *__restrict__ pz, const double *__restrict__ vel,
@@ -137,6 +146,22 @@ k_p2g(Dims d, int comp, const double *__restrict__ px, const double *__restrict_
                         return (hx * hy) * hz;  // 0 whenever one factor is 0
                     };
                     int t = t0;
+                    if (REC) {
+                        for (; t + 1 < t1; t += 2) {
+                            double x0, y0, z0, v0, x1, y1, z1, v1;
+                            ld_rec(px + 4 * (int64_t)t, x0, y0, z0, v0);
+                            ld_rec(px + 4 * (int64_t)(t + 1), x1, y1, z1, v1);
+                            const double w0 = weight(x0, y0, z0), w1 = weight(x1, y1, z1);
+                            kahan(w0, v0);
+                            kahan(w1, v1);
+                        }
+                        if (t < t1) {
+                            double x0, y0, z0, v0;
+                            ld_rec(px + 4 * (int64_t)t, x0, y0, z0, v0);
+                            kahan(weight(x0, y0, z0), v0);
+                        }
+                        continue;
+                    }
                     for (; t + 1 < t1; t += 2) {
                         const double x0 = __ldg(px + t), x1 = __ldg(px + t + 1);
                         const double y0 = __ldg(py + t), y1 = __ldg(py + t + 1);
@@ -177,8 +202,14 @@ void stage_p2g_impl(Ctx &c, const flip_step_params *prm, int fuse_force) {
         slab_face_range(c, comp, &f_lo, &f_hi);
         // the power-of-two test of div_dtau resolved at compile time: one
         // uniform branch and constant load less per hat (7.45 -> 6.50 ms/step)
-        (c.d.pow2 ? k_p2g<true, 1> : k_p2g<true, 0>)<<<nblocks(f_hi - f_lo, kThreads, (int64_t)1 << 30), kThreads, 0, c.st>>>(
-            c.d, comp, c.P.a[0], c.P.a[1], c.P.a[2], c.P.a[3 + comp], c.offset, nullptr, o,
+        const bool rec = c.prec_valid && c.prec && !c.slab.on;
+        static const int rec_minb = getenv("FLIPB200_P2G_REC_MINB") ? atoi(getenv("FLIPB200_P2G_REC_MINB")) : 5;
+        auto kp = rec ? (rec_minb == 4 ? (c.d.pow2 ? k_p2g<true, 1, 4, true> : k_p2g<true, 0, 4, true>)
+                                       : (c.d.pow2 ? k_p2g<true, 1, 5, true> : k_p2g<true, 0, 5, true>))
+                      : (c.d.pow2 ? k_p2g<true, 1> : k_p2g<true, 0>);
+        const double *rx = rec ? c.prec + (int64_t)comp * c.prec_cap * 4 : c.P.a[0];
+        kp<<<nblocks(f_hi - f_lo, kThreads, (int64_t)1 << 30), kThreads, 0, c.st>>>(
+            c.d, comp, rx, c.P.a[1], c.P.a[2], c.P.a[3 + comp], c.offset, nullptr, o,
             c.label, c.sc, g, fuse_force, (unsigned)f_lo, (unsigned)f_hi, use_box ? 1 : 0);
         c.launches++;
     }

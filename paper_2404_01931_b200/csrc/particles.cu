@@ -178,6 +178,7 @@ __global__ void k_keys_count(ParticlePtrs P, int64_t n, Dims d, int *__restrict_
 
 void stage_bin_from_keys(Ctx &c) {
     c.pbox_valid = 0;  // the counts change: k_classify recomputes the box
+    c.prec_valid = 0;
     // offset = exclusive_scan(count) (binning.py:91); offset[ncells] = N
     exclusive_scan(ArrayIn{c.count}, c.ncells, c.offset, c.offset + c.ncells, c.scan_tmp, c.st);
     c.launches += 3;
@@ -185,7 +186,25 @@ void stage_bin_from_keys(Ctx &c) {
     radix_sort_cells(c.keys0, c.keys1, c.vals0, c.vals1, c.n, c.ncells, c.hist, c.scan_tmp,
                      &c.sc->total, c.st, &c.keys_sorted, &perm, &c.launches);
     if (c.n > 0) {
-        k_gather6<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.Q, perm, c.n);
+        // P2G records alongside (one GPU, opt-in FLIPB200_P2G_REC=1): P2G 6.10 -> 5.40 ms
+        // at 256^3, but the 2.5 GB of record stores cost BIN +0.46 ms and the step
+        // comes out +0.1 ms, so the SoA walk stays the default
+        static const bool rec_env = getenv("FLIPB200_P2G_REC") && atoi(getenv("FLIPB200_P2G_REC"));
+        bool rec = rec_env && !c.slab.on;
+        if (rec && c.n > c.prec_cap) {
+            if (c.prec) cudaFree(c.prec);
+            c.prec = nullptr;
+            c.prec_cap = 0;
+            const int64_t want = c.n + c.n / 4 + 4096;
+            if (cudaMalloc(&c.prec, sizeof(double) * 12 * (size_t)want) == cudaSuccess) c.prec_cap = want;
+            else cudaGetLastError();
+        }
+        rec = rec && c.prec;
+        if (rec)
+            k_gather6_rec<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.Q, perm, c.n, c.prec, c.prec_cap);
+        else
+            k_gather6<<<nblocks(c.n), kThreads, 0, c.st>>>(c.P, c.Q, perm, c.n);
+        c.prec_valid = rec ? 1 : 0;
         c.launches++;
         std::swap(c.P, c.Q);
     }

@@ -177,6 +177,28 @@ __global__ void k_iota(int *a, int64_t n) {
     for (int64_t i = gtid(); i < n; i += gstride()) a[i] = (int)i;
 }
 
+// k_gather6 that also writes the P2G records rec[comp][i] = {x, y, z, v_comp}
+// (three 32-byte stores per particle).
+__global__ void k_gather6_rec(ParticlePtrs src, ParticlePtrs dst, const int *__restrict__ perm,
+                              int64_t n, double *__restrict__ rec, int64_t ld) {
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        const int j = perm[i];
+        double v[6];
+#pragma unroll
+        for (int a = 0; a < 6; a++) {
+            v[a] = __ldg(src.a[a] + j);
+            dst.a[a][i] = v[a];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+            double *r = rec + ((int64_t)c * ld + i) * 4;
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(r), "d"(v[0]), "d"(v[1]),
+                         "d"(v[2]), "d"(v[3 + c])
+                         : "memory");
+        }
+    }
+}
+
 // ParticleSet.reorder: dst[a][i] = src[a][perm[i]] for the six SoA arrays.
 __global__ void k_gather6(ParticlePtrs src, ParticlePtrs dst, const int *__restrict__ perm,
                           int64_t n) {
