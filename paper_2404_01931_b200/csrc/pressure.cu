@@ -332,8 +332,17 @@ __device__ __forceinline__ double pw_leaf8(const LD &ld, int64_t s, int64_t len,
     r = r + __shfl_xor_sync(mask, r, 1, 8);
     r = r + __shfl_xor_sync(mask, r, 2, 8);
     r = r + __shfl_xor_sync(mask, r, 4, 8);
-    if (g == 0)
-        for (int64_t i = m; i < len; i++) r += ld(s + i);
+    if (g == 0 && m < len) {
+        // the len % 8 tail in order; its loads issued together at a clamped
+        // (valid) index instead of one round trip per element
+        const int rem = (int)(len - m);
+        double tv[7];
+#pragma unroll
+        for (int k = 0; k < 7; k++) tv[k] = ld(s + min(m + k, len - 1));
+#pragma unroll
+        for (int k = 0; k < 7; k++)
+            if (k < rem) r += tv[k];
+    }
     return r;
 }
 
