@@ -4,6 +4,10 @@ MIC(0) sweep's mean launch time (flip_set_probe), bit-exactness digest of
 the final state (so variants can be compared for identical results).
 
     FLIPB200_QUAD=0 python tools/ab_step.py [res] [K] [W]
+
+AB_CAP=n sets the particle capacity (default: the 12-per-cell bound); AB_PAD_GB=g holds g GB
+of extra device memory (footprint / placement experiments: the MIC(0) sweep time moves by
+~1.5 % with the allocation layout).
 """
 import ctypes as C
 import hashlib
@@ -23,7 +27,9 @@ res = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 W = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 spec = P.SceneSpec(name="dam-break", res=res)
-st = P.make_scene(spec)
+st = P.make_scene(spec, capacity=int(os.environ.get("AB_CAP", "0")))
+_pad_gb = float(os.environ.get("AB_PAD_GB", "0"))  # footprint experiment: extra device memory held
+_pad = torch.empty(int(_pad_gb * 2**30), dtype=torch.uint8, device="cuda") if _pad_gb > 0 else None
 for _ in range(W):
     P.step(st, spec)
 check(LIB.flip_set_probe(st.device.ctx, 1))
