@@ -205,7 +205,7 @@ extern "C" void flip_destroy(flip_ctx *c) {
     }
     void *ptrs[] = {c->u, c->v, c->w, c->p,
                     c->label, c->uo, c->vo, c->wo, c->ku, c->kv, c->kw, c->ku1, c->kv1, c->kw1,
-                    c->count, c->offset, c->count2, c->offset2, c->nadd, c->keys0, c->keys1,
+                    c->count, c->offset, c->count2, c->offset2, c->nadd, c->emit_cells, c->keys0, c->keys1,
                     c->vals0, c->vals1, c->hist, c->scan_tmp, c->rowscan, c->isrow, c->parent,
                     c->has_air, c->cell_of_row, c->nbr, c->diagd, c->rhs, c->x, c->r, c->z, c->s,
                     c->q, c->tq, c->precon, c->xtmp, c->u64_scratch, c->lvl, c->lvl_rows,
@@ -288,6 +288,7 @@ extern "C" int flip_create(int device, int64_t nx, int64_t ny, int64_t nz, doubl
     ALLOC(c->count2, nc + 1);
     ALLOC(c->offset2, nc + 1);
     ALLOC(c->nadd, nc + 1);
+    ALLOC(c->emit_cells, nc + 1);
     ALLOC(c->keys0, capacity);
     ALLOC(c->keys1, capacity);
     ALLOC(c->vals0, capacity);

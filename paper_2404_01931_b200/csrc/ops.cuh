@@ -35,6 +35,7 @@ struct DevScalars {
     int x_it;                           // last iteration whose x += alpha s k_pcg_dir applied
     unsigned dir_ticket;                // k_pcg_dir's last-block ticket (re-armed to 0)
     int pbox_min[3], pbox_max[3];       // cells holding particles (k_classify), inclusive
+    int emit_n;                         // cells reseed refills (k_reseed_count's list)
 };
 
 // CUDA-event bracketing of one kernel class (bench roofline evidence).
@@ -119,6 +120,7 @@ struct Ctx {
             *kw1 = nullptr;
     int *count = nullptr, *offset = nullptr;  // offset has ncells + 1 entries
     int *count2 = nullptr, *offset2 = nullptr, *nadd = nullptr;  // reseed output hash
+    int *emit_cells = nullptr;         // cells reseed refills, in no particular order
     int *keys0 = nullptr, *keys1 = nullptr, *vals0 = nullptr, *vals1 = nullptr;
     int *keys_sorted = nullptr;  // cell of each binned particle (valid after BIN)
     int *hist = nullptr;

@@ -377,7 +377,8 @@ void launch_particle_cells(Ctx &c, int *out) {
 // Cells outside [c0, c1) (another rank's slab) are left alone.
 __global__ void k_reseed_count(const int *__restrict__ count, const uint8_t *__restrict__ label,
                                int64_t nc, int density, int *__restrict__ nadd,
-                               int *__restrict__ new_count, DevScalars *sc, int64_t c0, int64_t c1) {
+                               int *__restrict__ new_count, DevScalars *sc, int64_t c0, int64_t c1,
+                               int *__restrict__ emit_cells) {
     int target = density * density * density;
     if (target > MAX_PER_CELL) target = MAX_PER_CELL;
     int changed = 0;
@@ -388,6 +389,14 @@ __global__ void k_reseed_count(const int *__restrict__ count, const uint8_t *__r
             add = target - cnt > 0 ? target - cnt : 0;
         nadd[c] = add;
         new_count[c] = (cnt < MAX_PER_CELL ? cnt : MAX_PER_CELL) + add;
+        if (add > 0 && emit_cells) {  // the refill list (warp-aggregated append)
+            const unsigned am = __activemask();
+            const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&sc->emit_n, __popc(am));
+            base = __shfl_sync(am, base, leader);
+            emit_cells[base + __popc(am & ((1u << lane) - 1u))] = (int)c;
+        }
         changed |= (add > 0) | (cnt > MAX_PER_CELL);
     }
     changed = __any_sync(0xffffffffu, changed);
@@ -460,14 +469,46 @@ __global__ void k_reseed_emit(ParticlePtrs Q, Dims d, const int *__restrict__ co
     }
 }
 
+// k_reseed_emit over k_reseed_count's list of refilled cells: one thread per
+// cell, every thread busy (the per-cell scan left most lanes idle).  Output
+// slots are fixed by new_offset, so the list order does not matter.
+__global__ void k_reseed_emit_list(ParticlePtrs Q, Dims d, const int *__restrict__ count,
+                                   const int *__restrict__ nadd, const int *__restrict__ new_offset,
+                                   int density, uint64_t seed, const double *__restrict__ u,
+                                   const double *__restrict__ v, const double *__restrict__ w,
+                                   const DevScalars *sc, const int *__restrict__ cells) {
+    if (!sc->reseed_changed) return;
+    const int m = sc->emit_n;
+    for (int q = (int)gtid(); q < m; q += (int)gstride()) {
+        const int64_t c = cells[q];
+        const int add = nadd[c], cnt = count[c];
+        const int64_t base = (int64_t)new_offset[c] + cnt;  // cnt < 3 <= MAX_PER_CELL
+        for (int j = 0; j < add; j++) {
+            double px, py, pz, vx, vy, vz;
+            jitter_pos(d, c, cnt + j, density, seed, px, py, pz);
+            sample_vel(d, u, v, w, px, py, pz, vx, vy, vz);
+            const int64_t at = base + j;
+            Q.a[0][at] = px;
+            Q.a[1][at] = py;
+            Q.a[2][at] = pz;
+            Q.a[3][at] = vx;
+            Q.a[4][at] = vy;
+            Q.a[5][at] = vz;
+        }
+    }
+}
+
 int stage_reseed(Ctx &c, const flip_step_params &prm) {
     c.pbox_valid = 0;
     int *new_count = c.count2, *new_offset = c.offset2, *nadd = c.nadd;
     cudaMemsetAsync(&c.sc->reseed_changed, 0, sizeof(int), c.st);
+    static const bool list_env = !getenv("FLIPB200_RESEED_LIST") || atoi(getenv("FLIPB200_RESEED_LIST"));
+    int *list = list_env ? c.emit_cells : nullptr;
+    if (list) cudaMemsetAsync(&c.sc->emit_n, 0, sizeof(int), c.st);
     const int64_t c1 = c.slab_c1 < 0 ? c.ncells : c.slab_c1;
     k_reseed_count<<<nblocks(c.ncells), kThreads, 0, c.st>>>(c.count, c.label, c.ncells,
                                                              prm.density, nadd, new_count, c.sc,
-                                                             c.slab_c0, c1);
+                                                             c.slab_c0, c1, list);
     exclusive_scan(ArrayIn{new_count}, c.ncells, new_offset, new_offset + c.ncells, c.scan_tmp,
                    c.st);
     c.launches += 4;
@@ -493,9 +534,14 @@ int stage_reseed(Ctx &c, const flip_step_params &prm) {
                                                            new_offset, c.sc);
         c.launches++;
     }
-    k_reseed_emit<<<nblocks((c.ncells + 1) / 2), kThreads, 0, c.st>>>(c.Q, c.d, c.count, nadd, new_offset,
-                                                            prm.density, prm.reseed_seed, c.u, c.v,
-                                                            c.w, c.sc);
+    if (list)
+        k_reseed_emit_list<<<nblocks(c.ncells / 64 + 1, kThreads, 8), kThreads, 0, c.st>>>(
+            c.Q, c.d, c.count, nadd, new_offset, prm.density, prm.reseed_seed, c.u, c.v, c.w, c.sc,
+            list);
+    else
+        k_reseed_emit<<<nblocks((c.ncells + 1) / 2), kThreads, 0, c.st>>>(c.Q, c.d, c.count, nadd,
+                                                                new_offset, prm.density,
+                                                                prm.reseed_seed, c.u, c.v, c.w, c.sc);
     c.launches++;
     // the host swaps P<->Q and the hash buffers after reading reseed_changed
     return 0;

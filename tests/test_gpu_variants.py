@@ -42,6 +42,7 @@ VARIANTS = {
     "project_inline": {"FLIPB200_PROJECT_OVERLAP": "0"},
     "no_particle_box": {"FLIPB200_EXTRAP_BOX": "0", "FLIPB200_P2G_BOX": "0"},
     "zr_dot_8lane": {"FLIPB200_STAGED_ZR": "0"},
+    "reseed_cell_scan": {"FLIPB200_RESEED_LIST": "0"},
 }
 
 
