@@ -26,7 +26,7 @@ from paper_2404_01931_b200._lib import LIB, check
 res = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 W = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-spec = P.SceneSpec(name="dam-break", res=res)
+spec = P.SceneSpec(name="dam-break", res=res, precond=os.environ.get("AB_PRECOND", "mic0"))
 st = P.make_scene(spec, capacity=int(os.environ.get("AB_CAP", "0")))
 _pad_gb = float(os.environ.get("AB_PAD_GB", "0"))  # footprint experiment: extra device memory held
 _pad = torch.empty(int(_pad_gb * 2**30), dtype=torch.uint8, device="cuda") if _pad_gb > 0 else None
