@@ -15,7 +15,7 @@ the reference's own scene builder restated on the device (synthetic, seed 0).
             uploads particles + labels from pinned host memory, steps, and
             downloads the particles.
 * roofline  dominant kernel = the MIC(0) substitution sweeps (k_mic_quad,
-            forward + backward, ~54% of the step): algorithmic bytes (3 x 8 B
+            forward + backward, ~52% of the step): algorithmic bytes (3 x 8 B
             per row) over the measured per-launch time of every launch in
             the timed region.  The per-launch time comes from %globaltimer
             stamps the kernel writes itself (first CTA past its programmatic
