@@ -245,7 +245,9 @@ __global__ void __launch_bounds__(QT * QT + 32 * HW) k_mic_quad(LaneArgs A) {
         unsigned long long g;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
         trace[4 * tile + 0] = g;
-        trace[4 * tile + 3] = (unsigned long long)b << 16 | (unsigned)c;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        trace[4 * tile + 3] = (unsigned long long)smid << 32 | (unsigned long long)b << 16 | (unsigned)c;
     }
     auto lstep = [&](int s) { return REV ? nsteps - 1 - s : s; };
     const bool ydin = ry > 0, ydout = ry < CY - 1;

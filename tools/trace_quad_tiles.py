@@ -23,7 +23,8 @@ tr = st.device.debug_buffer("wave_trace", 32768, dtype=np.uint64).astype(np.int6
 t4 = tr[:4 * 4096].reshape(-1, 4)
 t4 = t4[t4[:, 1] > 0]
 t0 = t4[:, 0].min()
-b, c = t4[:, 3] >> 16, t4[:, 3] & 0xffff
+b, c = (t4[:, 3] >> 16) & 0xffff, t4[:, 3] & 0xffff
+smid = t4[:, 3] >> 32
 TB, TC = b.max() + 1, c.max() + 1
 ent, first, end = [(t4[:, k] - t0) / 1e3 for k in (0, 2, 1)]
 F = np.full((TB, TC), np.nan)
@@ -51,6 +52,27 @@ for i in range(TB):
             lag[i, j] = F[i, j] - max(p)
 print("start lag behind the later producer (us):")
 print(lag)
+# SM of each tile (%smid) and the lag split by whether a tile's later producer sits on the
+# same half of the SM ids (a proxy for the same die) or the other half
+SM = np.full((TB, TC), -1)
+SM[b, c] = smid
+half = int(os.environ.get("SM_HALF", "74"))
+print("SM id per tile:")
+print(SM)
+same, cross = [], []
+for i in range(TB):
+    for j in range(TC):
+        cand = []
+        if i > 0:
+            cand.append((F[i - 1, j], (i - 1, j)))
+        if j > 0:
+            cand.append((F[i, j - 1], (i, j - 1)))
+        if cand and not np.isnan(lag[i, j]):
+            pi, pj = max(cand)[1]
+            (same if (SM[i, j] < half) == (SM[pi, pj] < half) else cross).append(lag[i, j])
+if same and cross:
+    print(f"lag behind the later producer: same SM half {np.median(same):.2f} us (n={len(same)}), "
+          f"other half {np.median(cross):.2f} us (n={len(cross)})")
 print(f"median lag {np.nanmedian(lag):.2f} us; median busy span {np.nanmedian(E - F):.1f} us; "
       f"last tile first step {F[-1, -1]:.1f} us, end {E[-1, -1]:.1f} us")
 T0 = int(os.environ.get("FLIPB200_TRACE_TILE0", "0"))
